@@ -1,0 +1,440 @@
+"""Pins for the CPU oracle: values the paper / SPEC print, closed forms,
+invariants, special cases that reduce to textbook or library routines, brute
+force on tiny inputs, and central finite differences.  None of these re-types
+the oracle's own formula; each would fail on a plausible mistake (dropped
+term, wrong sign or index, transposed operand, off-by-one window).
+"""
+import bisect
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import Problem
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# --------------------------------------------------------------------------- Morton / Eq. 4
+@pytest.mark.parametrize("case", _gold("interleave.json"), ids=lambda c: c["cite"][:20])
+def test_interleave_golden(case):
+    assert oracle.interleave(case["g"], case["d"], case["b"]) == case["code"]
+    assert oracle.deinterleave(case["code"], case["d"], case["b"]) == case["g"]
+
+
+@pytest.mark.parametrize("d,b", [(1, 4), (2, 1), (2, 3), (2, 4), (3, 2), (3, 4)])
+def test_interleave_bijective_and_monotone(d, b):
+    """bijection onto [0, 2^(d b)) and coordinatewise monotone (exhaustive)."""
+    grid = list(itertools.product(range(2 ** b), repeat=d))
+    codes = {g: oracle.interleave(list(g), d, b) for g in grid}
+    assert sorted(codes.values()) == list(range(2 ** (d * b)))
+    for g in grid:
+        assert tuple(oracle.deinterleave(codes[g], d, b)) == g
+    if len(grid) <= 256:
+        for g, h in itertools.product(grid, repeat=2):
+            if all(x <= y for x, y in zip(g, h)):
+                assert codes[g] <= codes[h]
+
+
+@pytest.mark.parametrize("d,b", [(2, 3), (3, 2), (2, 4)])
+def test_dyadic_cell_locality(d, b):
+    """Consequence of Eq. 4: grid points sharing the top (b-s) bits of every
+    coordinate fill exactly the code interval [P*2^(d s), (P+1)*2^(d s))."""
+    for s in range(b + 1):
+        cells = {}
+        for g in itertools.product(range(2 ** b), repeat=d):
+            cells.setdefault(tuple(x >> s for x in g), []).append(oracle.interleave(list(g), d, b))
+        for prefix, codes in cells.items():
+            lo = min(codes)
+            assert lo % (2 ** (d * s)) == 0
+            assert sorted(codes) == list(range(lo, lo + 2 ** (d * s)))
+
+
+def test_interleave_d1_identity_and_plane_order():
+    rng = np.random.default_rng(1)
+    for v in rng.integers(0, 2 ** 32, size=50):
+        assert oracle.interleave([int(v)], 1, 32) == int(v)
+    # MSB plane of coordinate 0 is the code's top bit (Eq. 4, b_11 first)
+    assert oracle.interleave([1 << 20, 0, 0], 3, 21) == 1 << 62
+    assert oracle.interleave([0, 1 << 20, 0], 3, 21) == 1 << 61
+    assert oracle.interleave([1, 0, 0], 3, 21) == 1 << 2
+    assert oracle.interleave([0, 0, 1], 3, 21) == 1
+
+
+# --------------------------------------------------------------------------- quantiser
+@pytest.mark.parametrize("case", _gold("quantize.json"), ids=lambda c: str(c["x"]))
+def test_quantize_golden(case):
+    assert oracle.quantize(case["x"], case["lo"], case["hi"], case["b"]) == case["g"]
+
+
+def test_quantize_endpoints_every_b():
+    for b in range(1, 33):
+        assert oracle.quantize(-1.25, -1.25, 3.5, b) == 0
+        assert oracle.quantize(3.5, -1.25, 3.5, b) == 2 ** b - 1
+
+
+def test_fit_bounds_joint_and_widened():
+    """joint min/max over Q and K per dim; a constant column widens by 0.5."""
+    p = Problem(1, 1, 3, 2, 4, 1)
+    Q = np.array([[[[-1.0, 7.0], [0.0, 7.0], [2.0, 7.0]]]], np.float32)
+    K = np.array([[[[0.5, 7.0], [-3.0, 7.0], [1.0, 7.0]]]], np.float32)
+    lohi = oracle.fit_bounds(p, Q, K)
+    assert lohi[0, 0, 0].tolist() == [-3.0, 6.5]
+    assert lohi[0, 0, 1].tolist() == [2.0, 7.5]
+
+
+def test_encode_d1_order_preserving():
+    """for d = 1 sorting codes == sorting the raw values (ties only by quantisation)."""
+    rng = np.random.default_rng(2)
+    p = Problem(1, 1, 200, 1, 4, 1)
+    Q = rng.normal(size=(1, 1, 200, 1)).astype(np.float32)
+    K = rng.normal(size=(1, 1, 200, 1)).astype(np.float32)
+    qc, kc, _ = oracle.encode(p, Q, K)
+    x = np.concatenate([Q.ravel(), K.ravel()])
+    c = np.concatenate([qc.ravel(), kc.ravel()])
+    o = np.argsort(x, kind="stable")
+    assert np.all(np.diff(c[o].astype(np.float64)) >= 0)
+
+
+def test_encode_rejects_nonfinite_and_bad_bits():
+    p = Problem(1, 1, 4, 3, 4, 1)
+    Q = np.zeros((1, 1, 4, 3), np.float32)
+    K = np.zeros((1, 1, 4, 3), np.float32)
+    K[0, 0, 2, 1] = np.nan
+    with pytest.raises(oracle.OracleError):
+        oracle.encode(p, Q, K)
+    with pytest.raises(oracle.OracleError):
+        oracle.encode(Problem(1, 1, 4, 3, 4, 1, bits=22), Q, np.zeros_like(Q))
+
+
+# --------------------------------------------------------------------------- sort
+@pytest.mark.parametrize("case", _gold("sort.json"), ids=lambda c: c["cite"][:12])
+def test_sort_golden(case):
+    p = Problem(1, 1, case["N"], 1, 4, 1, chunk=case["M"])
+    scode, perm = oracle.sort(p, np.array(case["codes"], np.uint64).reshape(1, 1, -1))
+    assert scode.ravel().tolist() == case["scode"]
+    assert perm.ravel().tolist() == case["perm"]
+
+
+@pytest.mark.parametrize("causal", [1, 0])
+def test_sort_matches_python_sorted(causal):
+    """Definition: each run sorted by (code, position) == Python's sorted()."""
+    rng = np.random.default_rng(3)
+    N, M = 300, 64
+    codes = rng.integers(0, 40, size=N).astype(np.uint64)   # many duplicates
+    p = Problem(1, 1, N, 2, 4, 1, chunk=M, causal=causal)
+    scode, perm = oracle.sort(p, codes.reshape(1, 1, N))
+    runs = [(s, min(s + M, N)) for s in range(0, N, M)] if causal else [(0, N)]
+    for s, e in runs:
+        ref = sorted(((int(codes[j]), j) for j in range(s, e)))
+        assert [(int(c), int(j)) for c, j in zip(scode.ravel()[s:e], perm.ravel()[s:e])] == ref
+
+
+# --------------------------------------------------------------------------- candidate windows
+@pytest.mark.parametrize("case", _gold("windows.json"), ids=lambda c: c["cite"][:12])
+def test_window_golden(case):
+    run = case["run"]
+    pins = oracle.insertion_point(run, case["qcode"])
+    s, w = oracle.window_span(pins, len(run), case["W"])
+    assert run[s:s + w] == case["selected"]
+
+
+def test_insertion_point_is_bisect_left():
+    """D3: the insertion point is torch.searchsorted's default 'left' side == bisect_left."""
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        run = sorted(rng.integers(0, 50, size=int(rng.integers(1, 40))).tolist())
+        q = int(rng.integers(0, 55))
+        assert oracle.insertion_point(run, q) == bisect.bisect_left(run, q)
+
+
+def test_window_span_properties():
+    for length in range(1, 20):
+        for W in range(1, 25):
+            for pins in range(0, length + 1):
+                s, w = oracle.window_span(pins, length, W)
+                assert w == min(W, length) and 0 <= s and s + w <= length
+                if W <= length and W // 2 <= pins <= length - (W - W // 2):
+                    assert s == pins - W // 2     # centred when not clamped
+
+
+# --------------------------------------------------------------------------- selection
+def _brute_knn_numpy(Q, K, k, M, causal):
+    """Textbook brute force: f32 distances in the pinned left-to-right order, (D, j) lexicographic."""
+    N, dk = Q.shape
+    out = -np.ones((N, k), np.int32)
+    for i in range(N):
+        lim = (i // M) * M if causal else N
+        if lim == 0:
+            continue
+        t = Q[i][None, :] - K[:lim]
+        D = np.zeros(lim, np.float32)
+        for d in range(dk):
+            D = D + t[:, d] * t[:, d]
+        order = np.lexsort((np.arange(lim), D))[:k]
+        out[i, :len(order)] = order
+    return out
+
+
+@pytest.mark.parametrize("dk,causal", [(2, 1), (3, 1), (4, 1), (3, 0)])
+def test_window_covering_run_equals_bruteforce_knn(dk, causal):
+    """W >= M => every admissible key is a candidate => I_i is the exact chunk-causal kNN."""
+    rng = np.random.default_rng(5 + dk)
+    N, M, k = 96, 16, 6
+    p = Problem(1, 1, N, dk, 4, k, window=N if not causal else M, chunk=M, causal=causal)
+    Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    qc, kc, _ = oracle.encode(p, Q, K)
+    sc, pm = oracle.sort(p, kc)
+    idx = oracle.select(p, Q, K, qc, sc, pm)
+    ref = _brute_knn_numpy(Q[0, 0], K[0, 0], k, M, causal)
+    np.testing.assert_array_equal(idx[0, 0], ref)
+
+
+def test_d1_window_2k_is_exact_knn():
+    """S:255 (W = 2k form): in 1-D the k nearest admissible keys are contiguous in sorted
+    order around the insertion point, so the 2k window contains them."""
+    rng = np.random.default_rng(6)
+    for trial in range(10):
+        N, M, k = 128, 32, 5
+        p = Problem(1, 1, N, 1, 4, k, window=2 * k, chunk=M, causal=1)
+        Q = rng.normal(size=(1, 1, N, 1)).astype(np.float32)
+        K = rng.normal(size=(1, 1, N, 1)).astype(np.float32)
+        qc, kc, _ = oracle.encode(p, Q, K)
+        assert len(np.unique(np.concatenate([qc.ravel(), kc.ravel()]))) == 2 * N   # no collisions
+        sc, pm = oracle.sort(p, kc)
+        idx = oracle.select(p, Q, K, qc, sc, pm)
+        ref = _brute_knn_numpy(Q[0, 0], K[0, 0], k, M, 1)
+        np.testing.assert_array_equal(idx[0, 0], ref)
+
+
+@pytest.mark.parametrize("M,W,k", [(1, 2, 2), (4, 8, 3), (16, 4, 4), (7, 10, 9)])
+def test_selection_invariants(M, W, k):
+    """causality j < floor(i/M) M; |I_i| = min(k, m M) when W >= k; no duplicates;
+    entries ascending by (D, j)."""
+    rng = np.random.default_rng(7 + M)
+    N, dk = 90, 3
+    p = Problem(1, 1, N, dk, 4, k, window=W, chunk=M, causal=1)
+    Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    qc, kc, _ = oracle.encode(p, Q, K)
+    sc, pm = oracle.sort(p, kc)
+    idx = oracle.select(p, Q, K, qc, sc, pm)[0, 0]
+    for i in range(N):
+        m = i // M
+        sel = [j for j in idx[i] if j >= 0]
+        assert all(j < m * M for j in sel)
+        assert len(sel) == min(k, m * M)
+        assert len(set(sel)) == len(sel)
+        assert all(j == -1 for j in idx[i][len(sel):])
+        q = Q[0, 0, i]
+        D = [np.float32(0) + sum((q - K[0, 0, j]) ** 2, np.float32(0)) for j in sel]
+        keys = list(zip(D, sel))
+        assert keys == sorted(keys)
+    # chunk-0 queries select nothing
+    assert np.all(idx[:M] == -1)
+
+
+# --------------------------------------------------------------------------- Cauchy forward
+def _fwd_case(case, dv=3):
+    """Construct exact coordinates hitting the golden distances (d_k = 3, q at the origin)."""
+    exact = {0.0: (0, 0, 0), 1.0: (1, 0, 0), 1.5: (1, .5, .5), 0.75: (.5, .5, .5)}
+    keys = [exact[d] for d in case["D"]]
+    n = 1 + len(keys)
+    Q = np.zeros((1, 1, n, 3), np.float32)
+    K = np.zeros((1, 1, n, 3), np.float32)
+    for r, kk in enumerate(keys):
+        K[0, 0, 1 + r] = kk
+        if r == 1 and case["D"][0] == case["D"][1]:
+            K[0, 0, 1 + r] = (-1, -.5, .5)
+    rng = np.random.default_rng(8)
+    V = rng.normal(size=(1, 1, n, dv)).astype(np.float32)
+    k = len(keys)
+    idx = -np.ones((1, 1, n, k), np.int32)
+    idx[0, 0, 0] = np.arange(1, n)
+    p = Problem(1, 1, n, 3, dv, k, chunk=1, mean_slot=0)
+    return p, Q, K, V, idx
+
+
+@pytest.mark.parametrize("case", _gold("cauchy.json"), ids=lambda c: str(c["D"]))
+def test_cauchy_golden(case):
+    p, Q, K, V, idx = _fwd_case(case)
+    O, Z = oracle.forward(p, Q, K, V, case["eps"], idx)
+    assert Z[0, 0, 0] == pytest.approx(case["Z"], rel=1e-15)
+    expect = sum(a * V[0, 0, 1 + r].astype(np.float64) for r, a in enumerate(case["A"]))
+    np.testing.assert_allclose(O[0, 0, 0], expect, rtol=1e-14, atol=1e-15)
+
+
+def test_cauchy_ratio_law_and_simplex():
+    """A_a/A_b = (D_b + eps)/(D_a + eps); weights sum to 1 (constant V -> constant o);
+    o in the convex hull of the attended values."""
+    rng = np.random.default_rng(9)
+    N, dk, dv, k = 40, 3, 5, 6
+    p = Problem(1, 1, N, dk, dv, k, window=12, chunk=4, mean_slot=0)
+    Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    qc, kc, _ = oracle.encode(p, Q, K)
+    sc, pm = oracle.sort(p, kc)
+    idx = oracle.select(p, Q, K, qc, sc, pm)
+    eps = 0.3
+    # one-hot values read the weights back out
+    for i in (20, 33, 39):
+        sel = [j for j in idx[0, 0, i] if j >= 0]
+        A = []
+        for j in sel:
+            V = np.zeros((1, 1, N, dv), np.float32)
+            V[0, 0, j, 0] = 1.0
+            O, _ = oracle.forward(p, Q, K, V, eps, idx)
+            A.append(O[0, 0, i, 0])
+        D = [float(np.sum((Q[0, 0, i].astype(np.float64) - K[0, 0, j]) ** 2)) for j in sel]
+        assert sum(A) == pytest.approx(1.0, abs=1e-14)
+        for a in range(len(sel)):
+            for b in range(len(sel)):
+                assert A[a] / A[b] == pytest.approx((D[b] + eps) / (D[a] + eps), rel=1e-12)
+    V = np.full((1, 1, N, dv), 2.5, np.float32)
+    O, _ = oracle.forward(p, Q, K, V, eps, idx)
+    active = (idx[0, 0, :, 0] >= 0)
+    np.testing.assert_allclose(O[0, 0][active], 2.5, rtol=1e-14)
+    V = rng.normal(size=(1, 1, N, dv)).astype(np.float32)
+    O, _ = oracle.forward(p, Q, K, V, eps, idx)
+    for i in np.nonzero(active)[0]:
+        vals = V[0, 0, [j for j in idx[0, 0, i] if j >= 0]]
+        assert np.all(O[0, 0, i] <= vals.max(0) + 1e-12) and np.all(O[0, 0, i] >= vals.min(0) - 1e-12)
+
+
+def _dense_causal_cauchy(Q, K, V, eps):
+    """Independent O(N^2) form of S:337/S:379-382: M = 1, k, W >= N => every j < i plus the
+    inclusive-prefix-mean slot, softmax_c over all of them."""
+    Q = Q.astype(np.float64); K = K.astype(np.float64); V = V.astype(np.float64)
+    N = Q.shape[0]
+    cnt = np.arange(1, N + 1)[:, None]
+    Kb = np.cumsum(K, 0) / cnt
+    Vb = np.cumsum(V, 0) / cnt
+    D = ((Q[:, None, :] - K[None, :, :]) ** 2).sum(-1)
+    S = np.where(np.tril(np.ones((N, N), bool), -1), 1.0 / (D + eps), 0.0)
+    Smu = 1.0 / (((Q - Kb) ** 2).sum(-1) + eps)
+    Zs = S.sum(1) + Smu
+    return (S @ V + Smu[:, None] * Vb) / Zs[:, None], Zs
+
+
+def test_forward_dense_special_case():
+    rng = np.random.default_rng(10)
+    N, dk, dv = 48, 3, 7
+    p = Problem(1, 1, N, dk, dv, N, window=N, chunk=1, causal=1, mean_slot=1)
+    Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    V = rng.normal(size=(1, 1, N, dv)).astype(np.float32)
+    out = oracle.pipeline(p, Q, K, V, 0.5)
+    O_ref, Z_ref = _dense_causal_cauchy(Q[0, 0], K[0, 0], V[0, 0], 0.5)
+    np.testing.assert_allclose(out["O"][0, 0], O_ref, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(out["Z"][0, 0], Z_ref, rtol=1e-12)
+    assert out["O"][0, 0, 0] == pytest.approx(V[0, 0, 0].astype(np.float64), rel=1e-15)  # N=1 row: mean slot only
+
+
+def test_noncausal_mean_is_global():
+    rng = np.random.default_rng(11)
+    N, dk, dv = 20, 2, 3
+    p = Problem(1, 1, N, dk, dv, N, window=N, causal=0, mean_slot=1)
+    Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    V = rng.normal(size=(1, 1, N, dv)).astype(np.float32)
+    out = oracle.pipeline(p, Q, K, V, 0.5)
+    q, kk, v = (x[0, 0].astype(np.float64) for x in (Q, K, V))
+    D = ((q[:, None] - kk[None]) ** 2).sum(-1)
+    S = 1.0 / (D + 0.5)
+    Smu = 1.0 / (((q - kk.mean(0)) ** 2).sum(-1) + 0.5)
+    O_ref = (S @ v + Smu[:, None] * v.mean(0)) / (S.sum(1) + Smu)[:, None]
+    np.testing.assert_allclose(out["O"][0, 0], O_ref, rtol=1e-12, atol=1e-13)
+
+
+# --------------------------------------------------------------------------- backward
+def _grid_inputs(rng, shape, step=2.0 ** -12):
+    """Values on a 2^-12 grid so that x +- 2^-14 is exact in f32 (finite differences)."""
+    return (np.round(rng.normal(size=shape) / step) * step).astype(np.float32)
+
+
+def _small_problem(causal=1, mean_slot=1, seed=12):
+    rng = np.random.default_rng(seed)
+    N, dk, dv, k = 16, 3, 8, 4
+    p = Problem(1, 1, N, dk, dv, k, window=8, chunk=4, causal=causal, mean_slot=mean_slot)
+    Q = _grid_inputs(rng, (1, 1, N, dk))
+    K = _grid_inputs(rng, (1, 1, N, dk))
+    V = _grid_inputs(rng, (1, 1, N, dv))
+    dO = rng.normal(size=(1, 1, N, dv)).astype(np.float32)
+    qc, kc, _ = oracle.encode(p, Q, K)
+    sc, pm = oracle.sort(p, kc)
+    idx = oracle.select(p, Q, K, qc, sc, pm)
+    return p, Q, K, V, dO, idx
+
+
+@pytest.mark.parametrize("causal,mean_slot", [(1, 1), (1, 0), (0, 1)])
+def test_backward_matches_central_differences(causal, mean_slot):
+    """P:2006-2045 closed forms + mean-slot chain rule vs central FD of L = sum dO.O (I fixed)."""
+    p, Q, K, V, dO, idx = _small_problem(causal, mean_slot)
+    eps = 0.5
+    h = 2.0 ** -14
+
+    def loss(Q_, K_, V_, e):
+        O, _ = oracle.forward(p, Q_, K_, V_, e, idx)
+        return float(np.sum(O * dO.astype(np.float64)))
+
+    dQ, dK, dV, d_eps = oracle.backward(p, Q, K, V, eps, idx, dO)
+    for name, X, G in (("Q", Q, dQ), ("K", K, dK), ("V", V, dV)):
+        fd = np.zeros_like(G)
+        for pos in np.ndindex(X.shape):
+            Xp = X.copy(); Xp[pos] += h
+            Xm = X.copy(); Xm[pos] -= h
+            args_p = {"Q": Q, "K": K, "V": V}; args_p[name] = Xp
+            args_m = {"Q": Q, "K": K, "V": V}; args_m[name] = Xm
+            fd[pos] = (loss(args_p["Q"], args_p["K"], args_p["V"], eps)
+                       - loss(args_m["Q"], args_m["K"], args_m["V"], eps)) / (2 * h)
+        scale = np.abs(G).max()
+        np.testing.assert_allclose(G, fd, rtol=1e-5, atol=1e-6 * scale, err_msg=name)
+    fd_eps = (loss(Q, K, V, eps + h) - loss(Q, K, V, eps - h)) / (2 * h)
+    assert d_eps == pytest.approx(fd_eps, rel=1e-6)
+
+
+def test_backward_zero_upstream_and_single_slot():
+    p, Q, K, V, dO, idx = _small_problem()
+    dQ, dK, dV, d_eps = oracle.backward(p, Q, K, V, 0.5, idx, np.zeros_like(dO))
+    assert not dQ.any() and not dK.any() and not dV.any() and d_eps == 0.0
+    # S:328 single slot: A = 1 => v_j - o_i = 0 => dq_i = 0 and dv_j = dO_i
+    p1 = Problem(1, 1, 2, 3, 4, 1, chunk=1, mean_slot=0)
+    rng = np.random.default_rng(13)
+    Q1 = rng.normal(size=(1, 1, 2, 3)).astype(np.float32)
+    K1 = rng.normal(size=(1, 1, 2, 3)).astype(np.float32)
+    V1 = rng.normal(size=(1, 1, 2, 4)).astype(np.float32)
+    dO1 = rng.normal(size=(1, 1, 2, 4)).astype(np.float32)
+    idx1 = np.array([[[[-1], [0]]]], np.int32)
+    dQ, dK, dV, d_eps = oracle.backward(p1, Q1, K1, V1, 0.5, idx1, dO1)
+    assert np.all(dQ == 0) and np.all(dK == 0) and d_eps == 0.0
+    np.testing.assert_array_equal(dV[0, 0, 0], dO1[0, 0, 1].astype(np.float64))
+
+
+@pytest.mark.parametrize("causal", [1, 0])
+def test_backward_invariants(causal):
+    """Exact identities for fixed I (derived from Eq. 5): translation sum dq + sum dk = 0;
+    sum A = 1 => sum dv = sum dO; degree-0 homogeneity in (q, k, sqrt eps) =>
+    sum q.dq + sum k.dk + 2 eps deps = 0."""
+    rng = np.random.default_rng(14)
+    N, dk, dv, k = 200, 3, 16, 8
+    p = Problem(2, 1, N, dk, dv, k, window=16, chunk=25, causal=causal, mean_slot=1)
+    Q = rng.normal(size=(2, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(2, 1, N, dk)).astype(np.float32)
+    V = rng.normal(size=(2, 1, N, dv)).astype(np.float32)
+    dO = rng.normal(size=(2, 1, N, dv)).astype(np.float32)
+    eps = 0.5
+    out = oracle.pipeline(p, Q, K, V, eps, dO)
+    dQ, dK, dV = out["dQ"], out["dK"], out["dV"]
+    np.testing.assert_allclose(dQ.sum(2) + dK.sum(2), 0.0, atol=1e-12)
+    np.testing.assert_allclose(dV.sum(2), dO.astype(np.float64).sum(2), atol=1e-11)
+    euler = (Q * dQ).sum() + (K * dK).sum() + 2 * eps * out["d_eps"]
+    assert abs(euler) < 1e-11 * (np.abs(Q * dQ).sum() + 1)
