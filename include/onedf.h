@@ -1,0 +1,173 @@
+/*
+ * onedf.h -- C ABI of the B200-native (sm_100a) ZETA top-k attention hot path.
+ *
+ * ZETA / "1DFormer" (arXiv 2501.14577).  Citations: "P:n" = PAPER.md line n
+ * (final draft D unless noted), "S:n" = SPEC.md line n, "Dk" = reading k in
+ * DESIGN.md ("Readings").  The operation each entry point performs is defined
+ * in DESIGN.md section "Path" and, bit for bit / within the stated tolerance,
+ * by the CPU oracle under oracle/ (test infrastructure, never linked here).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * Ownership.  Every pointer except the onedf_problem* is CALLER-OWNED DEVICE
+ *   memory (allocated e.g. by PyTorch's caching allocator), except the
+ *   host-buffer entry point onedf_topk_attn_step_host which says otherwise.
+ *   The library never allocates, frees or synchronises.
+ * Layout.  Contiguous row-major, fastest in the last dimension:
+ *   Q, K            float  [B, H, N, d_k]
+ *   V, O, dO, dV    float  [B, H, N, d_v]
+ *   qcode, kcode    uint64 [B, H, N]        Morton codes (d_k*b bits used)
+ *   scode, perm     uint64 / int32 [B, H, N]  chunk-major sorted runs: run c
+ *                   occupies positions [c*M, min((c+1)*M, N)) of each (b,h)
+ *                   row, sorted by (code, original position); perm holds the
+ *                   original positions.  Non-causal: one run of N.
+ *   lohi            double [B, H, 2, d_k]   per-dim (lo[d_k], hi[d_k])
+ *   idx             int32  [B, H, N, k]     ascending by (D, j), -1 padded
+ *   Z               float  [B, H, N]        Cauchy normaliser incl. mean slot
+ * Streams.  Every launch goes on `stream` (a cudaStream_t; NULL = legacy
+ *   default stream).  No global mutable state: calls on different streams
+ *   with disjoint workspaces are thread-safe.
+ * Errors.  Argument checks are synchronous and happen before any launch:
+ *   ONEDF_ERR_INVALID_ARG   a field out of range (see onedf_validate) or a
+ *                           NULL required pointer;
+ *   ONEDF_ERR_WORKSPACE     ws_bytes < onedf_workspace_size(p, op) or ws NULL;
+ *   ONEDF_ERR_UNSUPPORTED   current device is not sm_100 (B200), or a size
+ *                           beyond what this build implements (see validate);
+ *   ONEDF_ERR_CUDA          a launch failed (cudaGetLastError).
+ *   Data errors detected on the device (non-finite Q/K in encode; eps <= 0 or
+ *   non-finite in fwd/bwd) set flag bits in the first 4 bytes of that call's
+ *   workspace; onedf_check_device_status(ws) synchronises the stream and
+ *   reports them as ONEDF_ERR_NONFINITE.  No exceptions cross the ABI.
+ * Determinism.  Every output is bitwise reproducible run to run: no float
+ *   atomics anywhere; every reduction has a fixed order.
+ */
+#ifndef ONEDF_H
+#define ONEDF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ONEDF_VERSION 100
+
+typedef struct CUstream_st* onedf_stream_t;   /* == cudaStream_t */
+
+typedef enum {
+    ONEDF_OK = 0,
+    ONEDF_ERR_INVALID_ARG = 1,
+    ONEDF_ERR_UNSUPPORTED = 2,
+    ONEDF_ERR_CUDA = 3,
+    ONEDF_ERR_NONFINITE = 4,
+    ONEDF_ERR_WORKSPACE = 5
+} onedf_status;
+
+/* The paper's problem statement (Alg. "KwData" P:1778: keys, sequence length
+ * N, chunk size M, top-k value k; Q, K in R^{B x N x d_K}, V in R^{B x N x d_V}
+ * P:1329; causal masks P:1335; trainable Cauchy scale P:1361). */
+typedef struct {
+    int64_t B, H, N;     /* batch, heads, positions; 1 <= N, N*k < 2^31            */
+    int32_t d_k, d_v;    /* 1 <= d_k <= 8 ; 4 <= d_v <= 256, d_v % 4 == 0             */
+    int32_t k;           /* 1 <= k <= 256 : neighbours kept (|I_q|)            */
+    int32_t window;      /* W >= k : candidates per sorted run; 0 -> 2k (D1)   */
+    int32_t chunk;       /* M >= 1 : causal chunk size; ignored if !causal    */
+    int32_t bits;        /* b : bits per dim, d_k*b <= 63, b <= 32; 0 -> min(63/d_k,32) */
+    int32_t causal;      /* 1: key j visible to query i iff j < floor(i/M)*M (D6); 0: all */
+    int32_t mean_slot;   /* 1: append the prefix-mean token (D8); 0: off      */
+} onedf_problem;
+
+enum {
+    ONEDF_OP_ENCODE = 0,
+    ONEDF_OP_SORT = 1,
+    ONEDF_OP_FWD = 2,
+    ONEDF_OP_BWD = 3,
+    ONEDF_OP_STEP_HOST = 4
+};
+
+/* Synchronous range checks of every field (no device work).  Also returns
+ * ONEDF_ERR_UNSUPPORTED when a sorted run would exceed the largest segment
+ * this build sorts (onedf_max_run_length()). */
+onedf_status onedf_validate(const onedf_problem* p);
+
+/* Longest sorted run (M causal, N non-causal) the segmented sort handles. */
+int64_t onedf_max_run_length(void);
+
+/* Bytes of device workspace `op` needs (0 if the problem is invalid).  The
+ * workspace must be 256-byte aligned; its contents need not be initialised. */
+size_t onedf_workspace_size(const onedf_problem* p, int op);
+
+/* A1 + A2: bounds and Morton encode (P:952-954 draft C quantiser, Eq. 4
+ * P:1276-1280 interleave, "Q_z, K_z = Z-order(Q), Z-order(K)").
+ *   lohi_in   NULL -> fit per (b,h) per dim jointly over Q and K, constant dims
+ *             widened by +-0.5 (D10); else caller-fixed bounds [B,H,2,d_k].
+ *   g = clamp(floor(((x - lo)/(hi - lo)) * (2^b - 1)), 0, 2^b - 1) in f64 (D9);
+ *   code = bit planes MSB first, coordinate 0 first within a plane (Eq. 4).
+ *   lohi_out  nullable; receives the bounds used.
+ * Non-finite Q/K -> NONFINITE flag (codes of such rows are unspecified). */
+onedf_status onedf_encode(const onedf_problem* p, const float* Q, const float* K,
+                          const double* lohi_in, uint64_t* qcode, uint64_t* kcode,
+                          double* lohi_out, void* ws, size_t ws_bytes, onedf_stream_t stream);
+
+/* A3: segmented stable sort of key codes ("torch.sort", "radix
+ * sorted", Alg. P:1786-1790 "divide the sorted keys into multiple chunks",
+ * S:215-223).  Each run sorted by (code, position); scode/perm chunk-major. */
+onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode,
+                        int32_t* perm, void* ws, size_t ws_bytes, onedf_stream_t stream);
+
+/* A4-A7: prefix means, causal candidate search, exact top-k, Cauchy weights
+ * and value gather (Eq. 5, Eq. 6).
+ *   For query i: for every admissible run c (c < floor(i/M), or the single
+ *   non-causal run): p_c = lower_bound(run_c, qcode_i) (D3), w = min(W, len),
+ *   s = min(max(p_c - floor(W/2), 0), len - w) (D2); candidates = union of
+ *   run_c[s, s+w).  I_i = first min(k, #candidates) by (D32, j) where D32 is
+ *   the f32 squared distance summed left to right without FMA (D23).
+ *   S_ij = 1/(||q_i - k_j||^2 + eps) (f64), mean slot S_imu with the inclusive
+ *   prefix means (D8), Z_i = sum S, o_i = sum (S/Z) v.  Chunk-0 queries with
+ *   mean_slot == 0: o = 0, Z = 0, idx = -1 (D7).
+ *   eps       device float scalar, eps > 0 and finite (else NONFINITE flag).
+ *   O, idx, Z outputs (idx/Z are what onedf_topk_attn_bwd consumes). */
+onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K,
+                                 const float* V, const float* eps, const uint64_t* qcode,
+                                 const uint64_t* scode, const int32_t* perm, float* O,
+                                 int32_t* idx, float* Z, void* ws, size_t ws_bytes,
+                                 onedf_stream_t stream);
+
+/* A8-A12: backward with I held fixed (D16), appendix P:2006-2045 with the
+ * dot-product reading D15, the mean-slot chain rule (S:323(a)) and one shared
+ * eps (D20).  dK/dV accumulate through a stable sort of (j, slot) pairs and
+ * fixed-order f64 segment sums -- no float atomics.
+ *   O, Z, idx  the forward's outputs for the same inputs.
+ *   dQ, dK, dV overwritten (f32); d_eps device DOUBLE scalar, overwritten with
+ *   the sum over all (b,h,i). */
+onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K,
+                                 const float* V, const float* eps, const float* O,
+                                 const float* dO, const int32_t* idx, const float* Z,
+                                 float* dQ, float* dK, float* dV, double* d_eps,
+                                 void* ws, size_t ws_bytes, onedf_stream_t stream);
+
+/* End-to-end training step from HOST buffers (the user-facing call the e2e
+ * metric times): async H2D copies of Q, K, V, dO (host pointers; pinned for
+ * full speed), then encode -> sort -> fwd -> bwd on the device, then async
+ * D2H copies of O, dQ, dK, dV (host pointers) and d_eps (host double*).
+ * eps is passed by value.  All device buffers live in `ws` (device,
+ * onedf_workspace_size(p, ONEDF_OP_STEP_HOST) bytes).  Returns after
+ * enqueueing; synchronise `stream` before reading the host outputs. */
+onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h,
+                                       const float* V_h, float eps, const float* dO_h,
+                                       float* O_h, float* dQ_h, float* dK_h, float* dV_h,
+                                       double* d_eps_h, void* ws, size_t ws_bytes,
+                                       onedf_stream_t stream);
+
+/* Synchronises `stream`, then reads the flag word of `ws` (a workspace
+ * previously passed to encode/fwd/bwd): ONEDF_OK or ONEDF_ERR_NONFINITE. */
+onedf_status onedf_check_device_status(const void* ws, onedf_stream_t stream);
+
+const char* onedf_status_string(onedf_status s);
+int onedf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ONEDF_H */

@@ -1,0 +1,15 @@
+"""onedf: B200-native (sm_100a) ZETA parallel causal top-k attention (arXiv 2501.14577).
+
+The hot path (Morton encode, segmented radix sort, causal candidate search,
+exact top-k, Adaptive Cauchy-Softmax gather, deterministic backward) lives in
+hand-written CUDA kernels behind the C ABI ``include/onedf.h``
+(``libonedf.so``); this package is its thin Python binding.
+"""
+from .abi import (OK, OP_BWD, OP_ENCODE, OP_FWD, OP_SORT, OP_STEP_HOST, OnedfError, Problem,  # noqa: F401
+                  onedf_check_device_status, onedf_encode, onedf_max_run_length, onedf_sort,
+                  onedf_topk_attn_bwd, onedf_topk_attn_fwd, onedf_topk_attn_step_host, onedf_validate,
+                  onedf_version, onedf_workspace_size, status_string)
+from .api import (HostStep, Workspace, ZetaTopkAttention, check_device_status, default_chunk,  # noqa: F401
+                  encode, make_problem, sort, topk_attn_bwd, topk_attn_fwd, zeta_attention)
+
+__version__ = "0.1.0"

@@ -1,0 +1,155 @@
+"""ctypes binding of libonedf.so -- argument marshalling only.
+
+Every function here has the same name and argument order as the C entry
+point in ``include/onedf.h``; tensors are passed as raw device pointers and
+the stream defaults to torch's current stream.  There is no fallback: if the
+shared library is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libonedf.so")
+
+OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NONFINITE, ERR_WORKSPACE = range(6)
+OP_ENCODE, OP_SORT, OP_FWD, OP_BWD, OP_STEP_HOST = range(5)
+
+
+class OnedfError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: onedf status {status} ({status_string(status)})")
+
+
+class Problem(ctypes.Structure):
+    """Mirror of ``onedf_problem`` (include/onedf.h)."""
+    _fields_ = [("B", ctypes.c_int64), ("H", ctypes.c_int64), ("N", ctypes.c_int64),
+                ("d_k", ctypes.c_int32), ("d_v", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("window", ctypes.c_int32), ("chunk", ctypes.c_int32), ("bits", ctypes.c_int32),
+                ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32)]
+
+    def __repr__(self):
+        return "Problem(" + ", ".join(f"{n}={getattr(self, n)}" for n, _ in self._fields_) + ")"
+
+    @property
+    def BH(self) -> int:
+        return self.B * self.H
+
+    @property
+    def W(self) -> int:
+        return self.window or 2 * self.k
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libonedf.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER(Problem)
+    vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+    sig = {
+        "onedf_validate": (i32, [P]),
+        "onedf_max_run_length": (ctypes.c_int64, []),
+        "onedf_workspace_size": (sz, [P, i32]),
+        "onedf_encode": (i32, [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_sort": (i32, [P, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_step_host": (i32, [P, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_check_device_status": (i32, [vp, vp]),
+        "onedf_status_string": (ctypes.c_char_p, [i32]),
+        "onedf_version": (i32, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTS = ("onedf_validate", "onedf_max_run_length", "onedf_workspace_size", "onedf_encode", "onedf_sort",
+           "onedf_topk_attn_fwd", "onedf_topk_attn_bwd", "onedf_topk_attn_step_host",
+           "onedf_check_device_status", "onedf_status_string", "onedf_version")
+
+
+def lib():
+    return _lib
+
+
+def status_string(s: int) -> str:
+    return _lib.onedf_status_string(s).decode()
+
+
+def _p(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return stream
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise OnedfError(st, where)
+
+
+def onedf_validate(p: Problem) -> int:
+    return _lib.onedf_validate(ctypes.byref(p))
+
+
+def onedf_max_run_length() -> int:
+    return _lib.onedf_max_run_length()
+
+
+def onedf_workspace_size(p: Problem, op: int) -> int:
+    return _lib.onedf_workspace_size(ctypes.byref(p), op)
+
+
+def onedf_encode(p, Q, K, lohi_in, qcode, kcode, lohi_out, ws, ws_bytes, stream=None):
+    _check(_lib.onedf_encode(ctypes.byref(p), _p(Q), _p(K), _p(lohi_in), _p(qcode), _p(kcode), _p(lohi_out),
+                             _p(ws), ws_bytes, _stream(stream)), "onedf_encode")
+
+
+def onedf_sort(p, kcode, scode, perm, ws, ws_bytes, stream=None):
+    _check(_lib.onedf_sort(ctypes.byref(p), _p(kcode), _p(scode), _p(perm), _p(ws), ws_bytes, _stream(stream)),
+           "onedf_sort")
+
+
+def onedf_topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, ws_bytes, stream=None):
+    _check(_lib.onedf_topk_attn_fwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode), _p(perm),
+                                    _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, _stream(stream)),
+           "onedf_topk_attn_fwd")
+
+
+def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, ws_bytes, stream=None):
+    _check(_lib.onedf_topk_attn_bwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx), _p(Z),
+                                    _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes, _stream(stream)),
+           "onedf_topk_attn_bwd")
+
+
+def onedf_topk_attn_step_host(p, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_h, dV_h, d_eps_h, ws, ws_bytes,
+                              stream=None):
+    _check(_lib.onedf_topk_attn_step_host(ctypes.byref(p), _p(Q_h), _p(K_h), _p(V_h), float(eps), _p(dO_h), _p(O_h),
+                                          _p(dQ_h), _p(dK_h), _p(dV_h), _p(d_eps_h), _p(ws), ws_bytes,
+                                          _stream(stream)),
+           "onedf_topk_attn_step_host")
+
+
+def onedf_check_device_status(ws, stream=None) -> int:
+    return _lib.onedf_check_device_status(_p(ws), _stream(stream))
+
+
+def onedf_version() -> int:
+    return _lib.onedf_version()

@@ -1,0 +1,149 @@
+"""Tensor-level API over the C ABI: allocation of outputs/workspace with
+PyTorch's caching allocator, and the autograd Function.  Every step of the
+path runs in libonedf.so's kernels; this file only marshals arguments.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import abi
+from .abi import Problem
+
+
+def make_problem(B, H, N, d_k, d_v, k, window=0, chunk=1, bits=0, causal=1, mean_slot=1) -> Problem:
+    p = Problem(B, H, N, d_k, d_v, k, window, chunk, bits, causal, mean_slot)
+    st = abi.onedf_validate(p)
+    if st != abi.OK:
+        raise abi.OnedfError(st, "onedf_validate")
+    return p
+
+
+def default_chunk(N: int) -> int:
+    """Reading D18: M = 256 until that would need more than 32 chunks, then 32 chunks."""
+    return 256 if N <= 256 * 32 else -(-N // 32)
+
+
+class Workspace:
+    """A reusable 256-B aligned device byte buffer (grown on demand)."""
+
+    def __init__(self, device=None):
+        self.device = torch.device(device or "cuda")
+        self._buf = None
+        self.nbytes = 0
+
+    def get(self, nbytes: int):
+        if self._buf is None or self.nbytes < nbytes:
+            self._buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+            self.nbytes = nbytes
+        off = (-self._buf.data_ptr()) % 256
+        return self._buf.data_ptr() + off, self.nbytes
+
+
+def _ws(p, op, ws):
+    need = abi.onedf_workspace_size(p, op)
+    if need == 0:
+        raise abi.OnedfError(abi.ERR_INVALID_ARG, "onedf_workspace_size")
+    ws = ws or Workspace()
+    return ws.get(need)
+
+
+def _dev(t: torch.Tensor, dtype=torch.float32):
+    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"expected a contiguous CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+    return t
+
+
+def encode(p: Problem, Q, K, lohi=None, ws: Workspace | None = None):
+    """A1+A2 -> (qcode, kcode, lohi); codes are int64 tensors holding the u64 bit patterns."""
+    Q, K = _dev(Q), _dev(K)
+    qcode = torch.empty((p.B, p.H, p.N), dtype=torch.int64, device=Q.device)
+    kcode = torch.empty_like(qcode)
+    lohi_out = torch.empty((p.B, p.H, 2, p.d_k), dtype=torch.float64, device=Q.device)
+    ptr, n = _ws(p, abi.OP_ENCODE, ws)
+    abi.onedf_encode(p, Q, K, None if lohi is None else _dev(lohi, torch.float64), qcode, kcode, lohi_out, ptr, n)
+    return qcode, kcode, lohi_out
+
+
+def sort(p: Problem, kcode, ws: Workspace | None = None):
+    """A3 -> (scode, perm)."""
+    kcode = _dev(kcode, torch.int64)
+    scode = torch.empty_like(kcode)
+    perm = torch.empty(kcode.shape, dtype=torch.int32, device=kcode.device)
+    ptr, n = _ws(p, abi.OP_SORT, ws)
+    abi.onedf_sort(p, kcode, scode, perm, ptr, n)
+    return scode, perm
+
+
+def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | None = None):
+    """A4-A7 -> (O, idx, Z)."""
+    Q, K, V, eps = _dev(Q), _dev(K), _dev(V), _dev(eps)
+    O = torch.empty((p.B, p.H, p.N, p.d_v), dtype=torch.float32, device=Q.device)
+    idx = torch.empty((p.B, p.H, p.N, p.k), dtype=torch.int32, device=Q.device)
+    Z = torch.empty((p.B, p.H, p.N), dtype=torch.float32, device=Q.device)
+    ptr, n = _ws(p, abi.OP_FWD, ws)
+    abi.onedf_topk_attn_fwd(p, Q, K, V, eps, _dev(qcode, torch.int64), _dev(scode, torch.int64),
+                            _dev(perm, torch.int32), O, idx, Z, ptr, n)
+    return O, idx, Z
+
+
+def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None):
+    """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor])."""
+    Q, K, V, eps, O, dO = _dev(Q), _dev(K), _dev(V), _dev(eps), _dev(O), _dev(dO)
+    dQ = torch.empty_like(Q)
+    dK = torch.empty_like(K)
+    dV = torch.empty_like(V)
+    d_eps = torch.empty((), dtype=torch.float64, device=Q.device)
+    ptr, n = _ws(p, abi.OP_BWD, ws)
+    abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32), _dev(Z), dQ, dK, dV, d_eps, ptr, n)
+    return dQ, dK, dV, d_eps
+
+
+def check_device_status(ws_ptr: int) -> int:
+    return abi.onedf_check_device_status(ws_ptr)
+
+
+class ZetaTopkAttention(torch.autograd.Function):
+    """o = ZETA(Q, K, V; eps) with gradients to Q, K, V and eps (indices held fixed, D16)."""
+
+    @staticmethod
+    def forward(ctx, Q, K, V, eps, p: Problem):
+        ws = Workspace(Q.device)
+        qcode, kcode, _ = encode(p, Q, K, ws=ws)
+        scode, perm = sort(p, kcode, ws=ws)
+        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps.reshape(()), qcode, scode, perm, ws=ws)
+        ctx.save_for_backward(Q, K, V, eps, O, idx, Z)
+        ctx.p = p
+        ctx.mark_non_differentiable(idx)
+        return O, idx
+
+    @staticmethod
+    def backward(ctx, dO, _didx):
+        Q, K, V, eps, O, idx, Z = ctx.saved_tensors
+        dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps.reshape(()), O, dO.contiguous(), idx, Z)
+        return dQ, dK, dV, d_eps.to(eps.dtype).reshape(eps.shape), None
+
+
+def zeta_attention(Q, K, V, eps, p: Problem):
+    return ZetaTopkAttention.apply(Q, K, V, eps, p)
+
+
+class HostStep:
+    """End-to-end call from pinned host buffers (onedf_topk_attn_step_host)."""
+
+    def __init__(self, p: Problem, device=None):
+        self.p = p
+        self.ws = Workspace(device)
+        self.need = abi.onedf_workspace_size(p, abi.OP_STEP_HOST)
+        self.ptr, _ = self.ws.get(self.need)
+
+    def __call__(self, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_h, dV_h, d_eps_h, stream=None):
+        abi.onedf_topk_attn_step_host(self.p, Q_h, K_h, V_h, eps, dO_h, O_h, dQ_h, dK_h, dV_h, d_eps_h, self.ptr,
+                                      self.need, stream)
+
+    @staticmethod
+    def h2d_bytes(p: Problem) -> int:
+        return 4 * p.BH * p.N * (2 * p.d_k + 2 * p.d_v)
+
+    @staticmethod
+    def d2h_bytes(p: Problem) -> int:
+        return 4 * p.BH * p.N * (2 * p.d_k + 2 * p.d_v) + 8

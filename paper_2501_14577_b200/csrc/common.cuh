@@ -1,0 +1,102 @@
+// common.cuh -- shared device helpers for the onedf sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "onedf.h"
+
+namespace onedf {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int WARP = 32;
+
+// Flag bits written into the first word of a workspace (see onedf.h "Errors").
+enum : unsigned { FLAG_NONFINITE_INPUT = 1u, FLAG_BAD_EPS = 2u };
+
+// Every workspace starts with this many bytes of header (flag word + pad).
+constexpr size_t WS_HEADER = 256;
+
+__host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Carves consecutive 256-B aligned regions out of a workspace.
+struct Carver {
+    char* base;
+    size_t off;
+    __host__ Carver(void* b) : base((char*)b), off(WS_HEADER) {}
+    template <typename T>
+    __host__ T* take(size_t count) {
+        off = align_up(off, 256);
+        T* p = base ? (T*)(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+    __host__ size_t bytes() const { return align_up(off, 256); }
+};
+
+// Record of one sorted key: d_k coordinates, the original position (int bits),
+// padded to a multiple of 4 floats so one run entry is 1-3 float4 loads.
+template <int DK>
+struct RecW { static constexpr int value = (DK + 1 + 3) / 4 * 4; };
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int src) {
+    return __shfl_sync(FULL, v, src);
+}
+
+// f32 ranking distance in the pinned order ((0 + t0^2) + t1^2) + ...; the
+// _rn intrinsics forbid FMA contraction (reading D23).
+template <int DK>
+__device__ __forceinline__ float rank_dist32(const float* q, const float* k) {
+    float acc = 0.f;
+#pragma unroll
+    for (int d = 0; d < DK; ++d) {
+        float t = __fsub_rn(q[d], k[d]);
+        acc = __fadd_rn(acc, __fmul_rn(t, t));
+    }
+    return acc;
+}
+
+// f64 squared distance used for the Cauchy weights (exact products of f32 data).
+template <int DK>
+__device__ __forceinline__ double dist64(const float* q, const float* k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < DK; ++d) {
+        double t = (double)q[d] - (double)k[d];
+        acc = fma(t, t, acc);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ void set_flag(void* ws, unsigned bit) {
+    atomicOr((unsigned*)ws, bit);
+}
+
+}  // namespace onedf
+
+#define ONEDF_DISPATCH_DK(dk, ...)                        \
+    switch (dk) {                                         \
+        case 1: { constexpr int DK = 1; __VA_ARGS__; } break; \
+        case 2: { constexpr int DK = 2; __VA_ARGS__; } break; \
+        case 3: { constexpr int DK = 3; __VA_ARGS__; } break; \
+        case 4: { constexpr int DK = 4; __VA_ARGS__; } break; \
+        case 5: { constexpr int DK = 5; __VA_ARGS__; } break; \
+        case 6: { constexpr int DK = 6; __VA_ARGS__; } break; \
+        case 7: { constexpr int DK = 7; __VA_ARGS__; } break; \
+        default: { constexpr int DK = 8; __VA_ARGS__; } break; \
+    }

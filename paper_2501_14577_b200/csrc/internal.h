@@ -1,0 +1,75 @@
+// internal.h -- launchers shared between the kernel translation units and abi.cu.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "onedf.h"
+
+namespace onedf {
+
+// Longest run the shared-memory segmented sort handles (keys + ping-pong in smem).
+constexpr int64_t SEG_SORT_MAX = 8192;
+
+int effective_bits(const onedf_problem* p);
+int effective_window(const onedf_problem* p);
+int64_t run_len_max(const onedf_problem* p);   // M (causal, capped at N) or N
+int64_t num_runs(const onedf_problem* p);
+
+// encode.cu
+size_t encode_ws_bytes(const onedf_problem* p, Carver* c);
+cudaError_t launch_encode(const onedf_problem* p, int b, const float* Q, const float* K, const double* lohi_in,
+                          uint64_t* qcode, uint64_t* kcode, double* lohi_out, void* ws, Carver* c,
+                          cudaStream_t st);
+
+// sort.cu
+cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode, int32_t* perm,
+                            cudaStream_t st);
+struct TransposeBufs {
+    uint32_t* keys[2];
+    uint32_t* vals[2];
+    uint32_t* hist;     // [BH][buckets][tiles]
+    int32_t* offsets;   // [BH][N+1]  CSR: slots of key j are sorted[off[j], off[j+1])
+    uint32_t* slots;    // final sorted slot ids (points into keys/vals)
+};
+void transpose_carve(const onedf_problem* p, Carver* c, TransposeBufs* t);
+cudaError_t launch_transpose(const onedf_problem* p, const int32_t* idx, TransposeBufs* t, cudaStream_t st);
+
+// mean.cu
+struct MeanBufs {
+    float* Kbar;        // [BH][rows][d_k], rows = N (causal) or 1
+    float* Vbar;        // [BH][rows][d_v]
+    double* part;       // scan partials
+};
+void mean_carve(const onedf_problem* p, Carver* c, MeanBufs* m);
+cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const float* V, MeanBufs* m,
+                                cudaStream_t st);
+// A11: dK_t += sum_{i>=t} wmu_i (q_i - Kbar_i)/(i+1), dV_t += sum_{i>=t} Amu_i dO_i/(i+1) (causal; 1/N all i otherwise)
+cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const float* dO, const float* muco,
+                                  MeanBufs* m, float* dK, float* dV, cudaStream_t st);
+
+// fwd.cu
+struct FwdBufs {
+    float* recs;        // [BH][N][RecW] sorted key records
+};
+void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f);
+cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
+                       const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
+                       float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st);
+
+// bwd.cu
+struct BwdBufs {
+    float2* coeff;      // [BH][N][k] (A, w)
+    float2* muco;       // [BH][N]    (A_mu, w_mu)
+    double* eps_part;   // [blocks]
+    int eps_blocks;
+};
+void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b);
+cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
+                       const float* O, const float* dO, const int32_t* idx, const float* Z, float* dQ, float* dK,
+                       float* dV, double* d_eps, const MeanBufs* m, BwdBufs* b, TransposeBufs* t, void* ws,
+                       cudaStream_t st);
+
+}  // namespace onedf

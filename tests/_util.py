@@ -1,0 +1,77 @@
+"""Shared helpers for the GPU parity tests: run the CUDA path (through the C
+ABI binding) and the CPU oracle on the same seeded synthetic inputs."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+import synth
+
+RTOL, ATOL = 1e-5, 1e-6          # north_star: fp32 outputs and gradients within 1e-5 rel / 1e-6 abs
+
+
+def gpu_run(kw: dict, x: dict, eps: float = synth.EPS, bwd: bool = True, lohi=None):
+    """Whole path on cuda:0 -> dict of numpy arrays (codes as uint64)."""
+    import torch
+
+    import paper_2501_14577_b200 as onedf
+    dev = torch.device("cuda:0")
+    t = {n: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for n, v in x.items()}
+    p = onedf.make_problem(**kw)
+    e = torch.tensor(eps, dtype=torch.float32, device=dev)
+    ws = onedf.Workspace(dev)
+    lohi_t = None if lohi is None else torch.from_numpy(lohi).to(dev)
+    qc, kc, lohi_out = onedf.encode(p, t["Q"], t["K"], lohi_t, ws=ws)
+    sc, pm = onedf.sort(p, kc, ws=ws)
+    O, idx, Z = onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws)
+    out = dict(qcode=qc, kcode=kc, lohi=lohi_out, scode=sc, perm=pm, O=O, idx=idx, Z=Z)
+    if bwd:
+        dQ, dK, dV, d_eps = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws)
+        out.update(dQ=dQ, dK=dK, dV=dV, d_eps=d_eps)
+    torch.cuda.synchronize()
+    res = {}
+    for n, v in out.items():
+        a = v.cpu().numpy()
+        res[n] = a.view(np.uint64) if n in ("qcode", "kcode", "scode") else a
+    return res
+
+
+def oracle_run(kw: dict, x: dict, eps: float = synth.EPS, bwd: bool = True, lohi=None):
+    p = oracle.Problem(**kw)
+    return oracle.pipeline(p, x["Q"], x["K"], x["V"], eps, x["dO"] if bwd else None, lohi)
+
+
+def assert_close(got, want, name: str, rtol=RTOL, atol=ATOL):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    assert got.shape == want.shape, (name, got.shape, want.shape)
+    err = np.abs(got - want)
+    bound = atol + rtol * np.abs(want)
+    bad = err > bound
+    if bad.any():
+        i = np.unravel_index(np.argmax(err - bound), err.shape)
+        raise AssertionError(f"{name}: {int(bad.sum())}/{bad.size} outside {rtol} rel / {atol} abs; "
+                             f"worst at {i}: got {got[i]!r} want {want[i]!r}")
+
+
+def assert_same(got, want, name: str):
+    got, want = np.asarray(got), np.asarray(want)
+    assert got.shape == want.shape, (name, got.shape, want.shape)
+    if not np.array_equal(got, want):
+        diff = np.argwhere(got != want)
+        i = tuple(diff[0])
+        raise AssertionError(f"{name}: {len(diff)} mismatching elements; first at {i}: got {got[i]} want {want[i]}")
+
+
+def slice_inputs(x: dict, bhs) -> dict:
+    """Select (b,h) slices of [B,H,N,.] arrays -> [1, len(bhs), N, .]."""
+    out = {}
+    for n, v in x.items():
+        flat = v.reshape(-1, *v.shape[2:])
+        out[n] = np.ascontiguousarray(flat[list(bhs)][None])
+    return out
+
+
+def slice_out(a, bhs):
+    flat = a.reshape(-1, *a.shape[2:])
+    return flat[list(bhs)][None]

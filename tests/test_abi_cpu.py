@@ -1,0 +1,112 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the
+header declares, the ctypes struct matches the C layout, and every argument
+check answers synchronously with the documented status (no GPU needed: all
+of these return before any launch)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "onedf.h")
+
+
+@pytest.fixture(scope="module")
+def onedf():
+    import __graft_entry__
+    __graft_entry__.build_cuda()
+    import paper_2501_14577_b200 as m
+    return m
+
+
+def _declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\*?\s+\*?(onedf_[a-z_0-9]+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared_functions()
+    for required in ("onedf_encode", "onedf_sort", "onedf_topk_attn_fwd", "onedf_topk_attn_bwd"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(onedf):
+    lib = ctypes.CDLL(onedf.abi.LIB_PATH)
+    for name in _declared_functions():
+        assert hasattr(lib, name), name
+    assert set(onedf.abi.EXPORTS) == set(_declared_functions())
+    assert onedf.onedf_version() == 100
+
+
+def test_struct_layout_matches_c(onedf, tmp_path):
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "onedf.h"\nint main(void){'
+                   'printf("%zu", sizeof(onedf_problem));'
+                   + "".join(f'printf(" %zu", offsetof(onedf_problem, {f}));' for f, _ in onedf.Problem._fields_)
+                   + "return 0;}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    vals = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert vals[0] == ctypes.sizeof(onedf.Problem)
+    assert vals[1:] == [getattr(onedf.Problem, f).offset for f, _ in onedf.Problem._fields_]
+
+
+GOOD = dict(B=2, H=3, N=1000, d_k=3, d_v=64, k=32, window=64, chunk=128, bits=0, causal=1, mean_slot=1)
+
+
+@pytest.mark.parametrize("field,value", [
+    ("d_k", 0), ("d_k", 9), ("d_v", 0), ("d_v", 6), ("d_v", 260), ("k", 0), ("k", 257), ("window", 16),
+    ("chunk", 0), ("bits", 22), ("bits", 33), ("causal", 2), ("mean_slot", -1), ("N", 0), ("B", 0),
+])
+def test_validate_rejects(onedf, field, value):
+    kw = dict(GOOD)
+    kw[field] = value
+    p = onedf.Problem(*kw.values())
+    assert onedf.onedf_validate(p) == onedf.abi.ERR_INVALID_ARG
+    assert onedf.onedf_workspace_size(p, onedf.OP_FWD) == 0
+
+
+def test_validate_accepts_and_sizes(onedf):
+    p = onedf.Problem(*GOOD.values())
+    assert onedf.onedf_validate(p) == onedf.OK
+    for op in (onedf.OP_ENCODE, onedf.OP_SORT, onedf.OP_FWD, onedf.OP_BWD, onedf.OP_STEP_HOST):
+        assert onedf.onedf_workspace_size(p, op) >= 256
+    # the backward holds coeff [BH, N, k] float2 at least
+    assert onedf.onedf_workspace_size(p, onedf.OP_BWD) >= 6 * 1000 * 32 * 8
+
+
+def test_run_length_limit_is_unsupported(onedf):
+    kw = dict(GOOD)
+    kw.update(N=4 * onedf.onedf_max_run_length(), chunk=2 * onedf.onedf_max_run_length())
+    assert onedf.onedf_validate(onedf.Problem(*kw.values())) == onedf.abi.ERR_UNSUPPORTED
+
+
+def test_calls_check_arguments_before_any_launch(onedf):
+    lib = onedf.abi.lib()
+    bad = onedf.Problem(*dict(GOOD, k=0).values())
+    good = onedf.Problem(*GOOD.values())
+    assert lib.onedf_encode(ctypes.byref(bad), 1, 1, None, 1, 1, None, 256, 1 << 30, None) == onedf.abi.ERR_INVALID_ARG
+    # workspace too small / misaligned / NULL -> ERR_WORKSPACE (checked before the device)
+    assert lib.onedf_topk_attn_fwd(ctypes.byref(good), *([256] * 10), 256, 16, None) == onedf.abi.ERR_WORKSPACE
+    assert lib.onedf_sort(ctypes.byref(good), 256, 256, 256, 257, 1 << 20, None) == onedf.abi.ERR_WORKSPACE
+    assert lib.onedf_topk_attn_bwd(ctypes.byref(good), *([256] * 12), None, 1 << 40, None) == onedf.abi.ERR_WORKSPACE
+    assert onedf.status_string(onedf.abi.ERR_WORKSPACE).startswith("workspace")
+
+
+def test_no_oracle_in_product_package():
+    """The product path never imports, links or calls the oracle, and vice versa."""
+    banned_product = ("import oracle", "from oracle", "oref_", "liboref")
+    pkg = os.path.join(ROOT, "paper_2501_14577_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                for b in banned_product:
+                    assert b not in text, (f, b)
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c")):
+            text = open(os.path.join(ROOT, "oracle", f)).read()
+            for b in ("import paper_2501_14577_b200", "from paper_2501_14577_b200", "libonedf", "onedf.h"):
+                assert b not in text, (f, b)
