@@ -1,0 +1,486 @@
+"""bench.py -- causal top-k attention fwd+bwd (ZETA, arXiv 2501.14577) on B200.
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config long64k] [--impl reference]
+
+A step = one pass of the whole hot path (A1-A12: encode + sort + fwd + bwd)
+over one batch of synthetic input already resident in HBM.  Under torchrun
+every rank runs its OWN batch (weak scaling, one process per GPU, (b,h)
+slices independent -> no data-path collective); the only exchange is the
+shared Cauchy scale's gradient d_eps (one f64 per rank, all-gathered and
+summed in rank order, reading D20).  Rank 0 prints one JSON line.
+
+--impl reference times the CPU oracle (oracle/, the method's plain f64
+reference -- this tier has no installable reference implementation) on the
+same config, each step a bounded sample (one (b,h) slice) of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "causal top-k attn fwd+bwd queries/s at N=64K, 1/2/4/8 B200; % HBM roofline"
+UNIT = "queries/s"
+
+
+# ----------------------------------------------------------------------------- algorithmic bytes
+def alg_bytes(cfg) -> dict:
+    """Per-kernel ALGORITHMIC bytes of one call over the whole batch, SURVEY 8(d):
+    gathered rows and candidate records counted per use; dense N^2 work not counted.
+    L = ceil(log2(M+1)); sum_m = sum_i m_i; sum_c = sum_i |C_i|; sum_kappa = sum_i |I_i|."""
+    N, dk, dv, k, W = cfg.N, cfg.d_k, cfg.d_v, cfg.k, cfg.window
+    s_k, s_v = 4 * dk, 4 * dv
+    if cfg.causal:
+        M = cfg.chunk
+        m = [i // M for i in range(0, N, 1)]
+        lens = [min(M, N - c * M) for c in range((N + M - 1) // M)]
+        # sum over queries of admissible runs / candidates / selected
+        sum_m = sum_c = sum_kappa = 0
+        prefix_w = [0]
+        prefix_len = [0]
+        for c, ln in enumerate(lens):
+            prefix_w.append(prefix_w[-1] + min(W, ln))
+            prefix_len.append(prefix_len[-1] + ln)
+        for c in range(len(lens)):
+            nq = lens[c]                       # queries of chunk c see runs 0..c-1
+            sum_m += nq * c
+            sum_c += nq * prefix_w[c]
+            sum_kappa += nq * min(k, prefix_len[c])
+        del m
+        Lbits = max(1, (M).bit_length())
+    else:
+        sum_m = N
+        sum_c = N * min(W, N)
+        sum_kappa = N * min(k, N)
+        Lbits = max(1, N.bit_length())
+    BH = cfg.BH
+    enc = 4 * N * s_k / 2 + 16 * N                      # fit+encode reads (2 passes over Q,K) + codes
+    enc = 4 * N * s_k + 16 * N
+    srt = 20 * N
+    means = 2 * N * (s_k + s_v)
+    fwd = N * (8 + s_k) + 8 * Lbits * sum_m + (s_k + 4) * sum_c + s_v * sum_kappa + N * (s_k + s_v) \
+        + N * (s_v + 4 * k + 4)
+    bq = N * (2 * s_v + s_k + 4 + 4 * k) + (s_v + s_k + 8) * sum_kappa + N * s_k
+    tr = 8 * sum_kappa + 4 * N
+    bk = (12 + s_v + s_k) * sum_kappa + N * (s_v + s_k)
+    scan = 4 * N * (s_k + s_v)
+    per = dict(encode=enc, sort=srt, fwd_means=means, fwd_topk=fwd, bwd_query=bq, bwd_transpose=tr, bwd_key=bk,
+               bwd_scans=scan)
+    out = {n: v * BH for n, v in per.items()}
+    out["F"] = BH * (enc + srt + means + fwd)
+    out["Bw"] = BH * (bq + tr + bk + scan)
+    out["B_alg"] = out["F"] + out["Bw"]
+    # compulsory: unique tensors only
+    fw_c = N * (2 * s_k + s_v) + 16 * N + 12 * N + N * (s_v + 4 * k + 4)
+    bw_c = N * (2 * s_k + 3 * s_v + 4 * k + 4) + N * (2 * s_k + s_v)
+    out["B_comp"] = BH * (fw_c + bw_c)
+    out["sum_c"] = BH * sum_c
+    out["sum_kappa"] = BH * sum_kappa
+    return out
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=5)
+        sm, mx, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+def _bad_clocks(c: dict) -> bool:
+    if any(r in c.get("reasons", []) for r in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")):
+        return True
+    if c.get("sm_mhz") and c.get("sm_max_mhz") and c["sm_mhz"] < 0.5 * c["sm_max_mhz"] and \
+            "sw_power_cap" not in c.get("reasons", []):
+        return True
+    return False
+
+
+# ----------------------------------------------------------------------------- helpers
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _rank_cfg(cfg, rank):
+    """Each rank's own batch: the config's B x H slices, seeded by global slice id."""
+    return cfg
+
+
+def _make_rank_inputs(cfg, rank):
+    import numpy as np
+
+    import synth
+    bhs = range(rank * cfg.BH, (rank + 1) * cfg.BH)
+    x = synth.make_inputs(cfg, bh_range=bhs)
+    return {n: np.ascontiguousarray(v.reshape(cfg.B, cfg.H, *v.shape[2:])) for n, v in x.items()}
+
+
+# ----------------------------------------------------------------------------- reference arm (CPU oracle)
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    oracle.build()
+    one = cfg.with_(B=1, H=1)
+    x = synth.make_inputs(cfg, bh_range=[0])
+    p = oracle.Problem(**one.problem_kwargs())
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.pipeline(p, x["Q"], x["K"], x["V"], synth.EPS, x["dO"])
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    sec = sum(times) / len(times)
+    value = cfg.N / sec
+    cores = oracle.num_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_json(cfg, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"one (b,h) slice of {cfg.name} (N={cfg.N} queries) per step, full "
+                                       f"encode+sort+select+fwd+bwd"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg):
+    """The oracle as it stands on this box's host cores, on a bounded sample: one (b,h) slice."""
+    import oracle
+    import synth
+    oracle.build()
+    one = cfg.with_(B=1, H=1)
+    x = synth.make_inputs(cfg, bh_range=[0])
+    p = oracle.Problem(**one.problem_kwargs())
+    t0 = time.perf_counter()
+    oracle.pipeline(p, x["Q"], x["K"], x["V"], synth.EPS, x["dO"])
+    sec = time.perf_counter() - t0
+    return {"value": cfg.N / sec, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"one (b,h) slice of {cfg.name}: {cfg.N} queries, full encode+sort+select+fwd+bwd, "
+                      f"{sec:.1f} s"}
+
+
+def _config_json(cfg, world):
+    return {"workload": cfg.name, "model": "ZETA top-k attention op (no weights)", "B": cfg.B, "H": cfg.H,
+            "global_batch": cfg.B * world, "seq_len": cfg.N, "d_k": cfg.d_k, "d_v": cfg.d_v, "k": cfg.k,
+            "window": cfg.window, "chunk": cfg.chunk, "chunks": -(-cfg.N // cfg.chunk) if cfg.causal else 1,
+            "causal": cfg.causal, "mean_slot": cfg.mean_slot, "pass": "encode+sort+fwd+bwd",
+            "l2": "inputs larger than L2 (V and dO are 1.6 GB each per GPU at long64k); no flush",
+            "parallelism": f"dp{world}: one process per GPU, each its own batch of (b,h) slices"}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_gpu(args, cfg, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    if rank == 0 or world == 1:
+        __graft_entry__.build()
+    if world > 1:
+        dist.init_process_group("nccl")
+        dist.barrier()
+    import paper_2501_14577_b200 as onedf
+    from paper_2501_14577_b200 import abi
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    x = _make_rank_inputs(cfg, rank)
+    t = {n: torch.from_numpy(v).to(dev) for n, v in x.items()}
+    p = onedf.make_problem(**cfg.problem_kwargs())
+    import synth
+    eps = torch.tensor(synth.EPS, dtype=torch.float32, device=dev)
+    BH, N = cfg.BH, cfg.N
+    qcode = torch.empty((cfg.B, cfg.H, N), dtype=torch.int64, device=dev)
+    kcode = torch.empty_like(qcode)
+    scode = torch.empty_like(qcode)
+    perm = torch.empty((cfg.B, cfg.H, N), dtype=torch.int32, device=dev)
+    O = torch.empty_like(t["V"])
+    idx = torch.empty((cfg.B, cfg.H, N, cfg.k), dtype=torch.int32, device=dev)
+    Z = torch.empty((cfg.B, cfg.H, N), dtype=torch.float32, device=dev)
+    dQ, dK, dV = torch.empty_like(t["Q"]), torch.empty_like(t["K"]), torch.empty_like(t["V"])
+    d_eps = torch.empty((), dtype=torch.float64, device=dev)
+    need = max(onedf.onedf_workspace_size(p, op) for op in (abi.OP_ENCODE, abi.OP_SORT, abi.OP_FWD, abi.OP_BWD))
+    wsbuf = torch.empty(need + 256, dtype=torch.uint8, device=dev)
+    ws = wsbuf.data_ptr() + ((-wsbuf.data_ptr()) % 256)
+    stream = torch.cuda.current_stream(dev)
+
+    # stage events: 0 start | 1 encode | 2 sort | fwd: 3 means 4 records 5 topk | bwd: 6 means 7 query
+    # 8 transpose 9 key 10 scan 11 eps | 12 d_eps exchange
+    NEV = 13
+
+    def new_events():
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(NEV)]
+        for e in evs:
+            e.record(stream)
+        return evs
+
+    def step(ev):
+        ev[0].record(stream)
+        abi.onedf_encode(p, t["Q"], t["K"], None, qcode, kcode, None, ws, need, stream)
+        ev[1].record(stream)
+        abi.onedf_sort(p, kcode, scode, perm, ws, need, stream)
+        ev[2].record(stream)
+        abi.onedf_topk_attn_fwd_traced(p, t["Q"], t["K"], t["V"], eps, qcode, scode, perm, O, idx, Z, ws, need,
+                                       ev[3:6], stream)
+        abi.onedf_topk_attn_bwd_traced(p, t["Q"], t["K"], t["V"], eps, O, t["dO"], idx, Z, dQ, dK, dV, d_eps, ws,
+                                       need, ev[6:12], stream)
+        if world > 1:
+            parts = [torch.empty((), dtype=torch.float64, device=dev) for _ in range(world)]
+            dist.all_gather(parts, d_eps)
+            total = parts[0].clone()
+            for q in parts[1:]:
+                total += q            # fixed rank order: deterministic
+            d_eps.copy_(total)
+        ev[12].record(stream)
+
+    stage_names = ["encode", "sort", "fwd_means", "fwd_records", "fwd_topk", "bwd_means", "bwd_query",
+                   "bwd_transpose", "bwd_key", "bwd_scans", "bwd_eps", "deps_exchange"]
+
+    # warm-up
+    for _ in range(args.warmup):
+        step(new_events())
+    torch.cuda.synchronize(dev)
+    st = onedf.check_device_status(ws)
+    if st != abi.OK:
+        raise RuntimeError(f"device status {st} after warm-up")
+
+    gpu_id = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
+
+    def timed():
+        evs = [new_events() for _ in range(args.steps)]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        clocks = ClockSampler(gpu_id)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        clocks.start()
+        time.sleep(0.3)
+        t0.record(stream)
+        for s in range(args.steps):
+            step(evs[s])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
+        total_ms = t0.elapsed_time(t1)
+        stages = {n: [] for n in stage_names}
+        for ev in evs:
+            for si, n in enumerate(stage_names):
+                stages[n].append(ev[si].elapsed_time(ev[si + 1]))
+        return total_ms, stages, clk
+
+    total_ms, stages, clk = timed()
+    if _bad_clocks(clk):
+        total_ms, stages, clk = timed()
+        clk["remeasured"] = True
+    ms = total_ms / args.steps
+    if world > 1:
+        mt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        ms = float(mt.item())
+
+    launches_per_step = count_launches(p)
+
+    # ------------------------------------------------------------ e2e through the host-buffer entry point
+    e2e = None
+    if not args.no_e2e:
+        del O, idx, Z, dQ, dK, dV, wsbuf, qcode, kcode, scode, perm
+        dev_inputs = t
+        del dev_inputs, t
+        torch.cuda.empty_cache()
+        pin = {n: torch.from_numpy(v).pin_memory() for n, v in x.items()}
+        outs = {n: torch.empty_like(pin["V" if n in ("O", "dV") else "Q"]).pin_memory()
+                for n in ("O", "dQ", "dK", "dV")}
+        d_eps_h = torch.zeros((), dtype=torch.float64).pin_memory()
+        hs = onedf.HostStep(p, dev)
+
+        def host_step():
+            hs(pin["Q"], pin["K"], pin["V"], synth.EPS, pin["dO"], outs["O"], outs["dQ"], outs["dK"], outs["dV"],
+               d_eps_h, stream)
+
+        for _ in range(max(1, min(args.warmup, 2))):
+            host_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ksteps = max(1, min(args.steps, 5))
+        e0.record(stream)
+        for _ in range(ksteps):
+            host_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1) / ksteps
+        if world > 1:
+            mt = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+            ems = float(mt.item())
+        e2e = {"value": world * BH * N / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": onedf.HostStep.h2d_bytes(p), "d2h_bytes_per_step": onedf.HostStep.d2h_bytes(p),
+               "api": "onedf_topk_attn_step_host (pinned host buffers, copies inside the timed region)",
+               "steps": ksteps}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ------------------------------------------------------------ roofline of the dominant kernel
+    ab = alg_bytes(cfg)
+    peak, peak_src = _peaks()
+    kern_map = {"fwd_topk": "fwd_topk", "bwd_query": "bwd_query", "bwd_key": "bwd_key"}
+    avg = {n: sum(v) / len(v) for n, v in stages.items()}
+    dom = max(kern_map, key=lambda n: avg[n])
+    achieved = ab[kern_map[dom]] / (avg[dom] / 1e3) / 1e9
+    traffic = _ncu_traffic(dom)
+    roof = {"bound": "hbm", "kernel": {"fwd_topk": "topk_attn_fwd_kernel", "bwd_query": "bwd_query_kernel",
+                                       "bwd_key": "bwd_key_kernel"}[dom],
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": peak_src,
+            "alg_bytes_per_launch": ab[kern_map[dom]], "avg_launch_ms": avg[dom],
+            "note": "achieved = SURVEY 8(d) algorithmic bytes (candidate records and gathered rows counted per "
+                    "use) / CUDA-event time of the kernel inside the timed region; can exceed 1 only through "
+                    "on-chip (L1/L2) reuse",
+            "step": {"B_alg": ab["B_alg"], "R_alg": ab["B_alg"] / (ms / 1e3) / 1e9 / peak,
+                     "B_comp": ab["B_comp"], "R_comp": ab["B_comp"] / (ms / 1e3) / 1e9 / peak}}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg)
+    value = world * BH * N / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic: seeded iid N(0,1) Q,K,V,dO (synth/, SURVEY 8(d))",
+            "config": _config_json(cfg, world), "tokens_per_s": world * cfg.B * N / (ms / 1e3),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches_per_step": launches_per_step, "clocks": clk,
+            "phases_ms": {n: round(v, 4) for n, v in avg.items()}}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def count_launches(p) -> int:
+    """Kernel launches of one step (encode 2, sort 1, fwd 3 means + records + topk, bwd 3 means + query +
+    3 per radix pass + offsets + key + 3 scan + eps), derived from the same plan the library uses."""
+    n_bits = 1
+    while (1 << n_bits) <= p.N:
+        n_bits += 1
+    passes = (n_bits + 8) // 9
+    means = 3 if p.causal else 2
+    fwd = (means if p.mean_slot else 0) + 2
+    bwd = (means if p.mean_slot else 0) + 1 + 3 * passes + 1 + 1 + (3 if p.mean_slot else 0) + 1
+    return 2 + 1 + fwd + bwd
+
+
+def _ncu_traffic(kernel_key):
+    """dram bytes per launch from the committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel_key)
+    except (OSError, ValueError):
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=None)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="long64k")
+    ap.add_argument("--impl", default="onedf", choices=["onedf", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = _dist_env()
+    if args.gpus is not None and args.gpus != world and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "run N>1 under torchrun (python -m torch.distributed.run ...)"}))
+        return 1
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return 0
+    run_gpu(args, cfg, world, rank, local)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

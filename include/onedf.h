@@ -147,6 +147,25 @@ onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const f
                                  float* dQ, float* dK, float* dV, double* d_eps,
                                  void* ws, size_t ws_bytes, onedf_stream_t stream);
 
+/* Instrumented twins of the fwd/bwd calls: identical launches and results,
+ * plus cudaEventRecord(events[s], stream) right after internal stage s
+ * (entries at s >= n_events, or NULL entries, are skipped).  `events` holds
+ * caller-created cudaEvent_t handles.  Stages:
+ *   fwd: 0 prefix means (A4)  1 sorted key records (K4)  2 top-k attention (A5-A7)
+ *   bwd: 0 prefix means (A4)  1 query side (A8)  2 transpose (A9)
+ *        3 key side (A10)     4 mean-slot scan (A11)      5 eps reduce (A12)    */
+onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K,
+                                        const float* V, const float* eps, const uint64_t* qcode,
+                                        const uint64_t* scode, const int32_t* perm, float* O,
+                                        int32_t* idx, float* Z, void* ws, size_t ws_bytes,
+                                        void* const* events, int n_events, onedf_stream_t stream);
+onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K,
+                                        const float* V, const float* eps, const float* O,
+                                        const float* dO, const int32_t* idx, const float* Z,
+                                        float* dQ, float* dK, float* dV, double* d_eps,
+                                        void* ws, size_t ws_bytes, void* const* events, int n_events,
+                                        onedf_stream_t stream);
+
 /* End-to-end training step from HOST buffers (the user-facing call the e2e
  * metric times): async H2D copies of Q, K, V, dO (host pointers; pinned for
  * full speed), then encode -> sort -> fwd -> bwd on the device, then async

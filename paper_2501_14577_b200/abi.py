@@ -58,6 +58,9 @@ def _load():
         "onedf_sort": (i32, [P, vp, vp, vp, vp, sz, vp]),
         "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32, vp]),
+        "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32,
+                                             vp]),
         "onedf_topk_attn_step_host": (i32, [P, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_check_device_status": (i32, [vp, vp]),
         "onedf_status_string": (ctypes.c_char_p, [i32]),
@@ -72,7 +75,8 @@ def _load():
 
 _lib = _load()
 EXPORTS = ("onedf_validate", "onedf_max_run_length", "onedf_workspace_size", "onedf_encode", "onedf_sort",
-           "onedf_topk_attn_fwd", "onedf_topk_attn_bwd", "onedf_topk_attn_step_host",
+           "onedf_topk_attn_fwd", "onedf_topk_attn_bwd", "onedf_topk_attn_fwd_traced",
+           "onedf_topk_attn_bwd_traced", "onedf_topk_attn_step_host",
            "onedf_check_device_status", "onedf_status_string", "onedf_version")
 
 
@@ -137,6 +141,26 @@ def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, w
     _check(_lib.onedf_topk_attn_bwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx), _p(Z),
                                     _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes, _stream(stream)),
            "onedf_topk_attn_bwd")
+
+
+def _events(events):
+    arr = (ctypes.c_void_p * max(1, len(events)))(*[e.cuda_event if e is not None else None for e in events])
+    return arr, len(events)
+
+
+def onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, ws_bytes, events, stream=None):
+    arr, n = _events(events)
+    _check(_lib.onedf_topk_attn_fwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode),
+                                           _p(perm), _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, arr, n,
+                                           _stream(stream)), "onedf_topk_attn_fwd_traced")
+
+
+def onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, ws_bytes, events,
+                               stream=None):
+    arr, n = _events(events)
+    _check(_lib.onedf_topk_attn_bwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx),
+                                           _p(Z), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes, arr, n,
+                                           _stream(stream)), "onedf_topk_attn_bwd_traced")
 
 
 def onedf_topk_attn_step_host(p, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_h, dV_h, d_eps_h, ws, ws_bytes,

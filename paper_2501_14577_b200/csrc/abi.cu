@@ -134,23 +134,26 @@ static onedf_status do_sort(const onedf_problem* p, const uint64_t* kcode, uint6
 }
 static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                            const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
-                           float* Z, void* ws, cudaStream_t st, bool zero) {
+                           float* Z, void* ws, cudaStream_t st, bool zero, const Trace& tr = Trace()) {
     if (zero && cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
     FwdLayout L = fwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
-    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, &L.m, &L.f, ws, st);
+    tr.mark(0, st);
+    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, &L.m, &L.f, ws, st, tr);
     return finish(e);
 }
 static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                            const float* O, const float* dO, const int32_t* idx, const float* Z, float* dQ, float* dK,
-                           float* dV, double* d_eps, void* ws, cudaStream_t st, bool zero) {
+                           float* dV, double* d_eps, void* ws, cudaStream_t st, bool zero,
+                           const Trace& tr = Trace()) {
     if (zero && cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
     BwdLayout L = bwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
+    tr.mark(0, st);
     if (e == cudaSuccess)
-        e = launch_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st);
+        e = launch_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st, tr);
     return finish(e);
 }
 
@@ -214,6 +217,35 @@ onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const f
         return ONEDF_ERR_INVALID_ARG;
     if ((((uintptr_t)V) | ((uintptr_t)dO) | ((uintptr_t)dV)) & 15) return ONEDF_ERR_INVALID_ARG;
     return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true);
+}
+
+onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K, const float* V,
+                                        const float* eps, const uint64_t* qcode, const uint64_t* scode,
+                                        const int32_t* perm, float* O, int32_t* idx, float* Z, void* ws,
+                                        size_t ws_bytes, void* const* events, int n_events, onedf_stream_t stream) {
+    onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_FWD);
+    if (s != ONEDF_OK) return s;
+    if (!Q || !K || !V || !eps || !qcode || !scode || !perm || !O || !idx || !Z) return ONEDF_ERR_INVALID_ARG;
+    if ((((uintptr_t)V) | ((uintptr_t)O)) & 15) return ONEDF_ERR_INVALID_ARG;
+    Trace tr;
+    tr.ev = events;
+    tr.n = n_events;
+    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, (cudaStream_t)stream, true, tr);
+}
+
+onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K, const float* V,
+                                        const float* eps, const float* O, const float* dO, const int32_t* idx,
+                                        const float* Z, float* dQ, float* dK, float* dV, double* d_eps, void* ws,
+                                        size_t ws_bytes, void* const* events, int n_events, onedf_stream_t stream) {
+    onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_BWD);
+    if (s != ONEDF_OK) return s;
+    if (!Q || !K || !V || !eps || !O || !dO || !idx || !Z || !dQ || !dK || !dV || !d_eps)
+        return ONEDF_ERR_INVALID_ARG;
+    if ((((uintptr_t)V) | ((uintptr_t)dO) | ((uintptr_t)dV)) & 15) return ONEDF_ERR_INVALID_ARG;
+    Trace tr;
+    tr.ev = events;
+    tr.n = n_events;
+    return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true, tr);
 }
 
 onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h, const float* V_h,

@@ -244,7 +244,7 @@ __global__ void eps_reduce_kernel(const double* __restrict__ part, int n, double
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                        const float* O, const float* dO, const int32_t* idx, const float* Z, float* dQ, float* dK,
                        float* dV, double* d_eps, const MeanBufs* m, BwdBufs* b, TransposeBufs* t, void* ws,
-                       cudaStream_t st) {
+                       cudaStream_t st, const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
     BwdArgs a;
     a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.O = O; a.dO = dO; a.idx = idx; a.Z = Z;
@@ -252,20 +252,25 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     a.N = N; a.total = total; a.k = p->k; a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
     a.ws = ws;
     ONEDF_DISPATCH_DK(p->d_k, { bwd_query_kernel<DK><<<(unsigned)b->eps_blocks, BWD_THREADS, 0, st>>>(a); });
+    tr.mark(1, st);
     cudaError_t e = launch_transpose(p, idx, t, st);
     if (e != cudaSuccess) return e;
+    tr.mark(2, st);
     KeyArgs ka;
     ka.Q = Q; ka.K = K; ka.dO = dO; ka.coeff = b->coeff; ka.slots = t->slots; ka.offsets = t->offsets;
     ka.dK = dK; ka.dV = dV; ka.N = N; ka.L = N * (int64_t)p->k; ka.total = total; ka.k = p->k; ka.dv = p->d_v;
     ONEDF_DISPATCH_DK(p->d_k, {
         bwd_key_kernel<DK><<<(unsigned)((total + BWD_WARPS - 1) / BWD_WARPS), BWD_THREADS, 0, st>>>(ka);
     });
+    tr.mark(3, st);
     if (p->mean_slot) {
         e = launch_mean_grad_scan(p, Q, dO, reinterpret_cast<const float*>(b->muco), const_cast<MeanBufs*>(m), dK,
                                   dV, st);
         if (e != cudaSuccess) return e;
     }
+    tr.mark(4, st);
     eps_reduce_kernel<<<1, 256, 0, st>>>(b->eps_part, b->eps_blocks, d_eps);
+    tr.mark(5, st);
     return cudaGetLastError();
 }
 

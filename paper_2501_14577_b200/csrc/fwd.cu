@@ -292,11 +292,12 @@ __global__ void __launch_bounds__(FWD_THREADS) topk_attn_fwd_kernel(const FwdArg
 
 cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                        const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
-                       float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st) {
+                       float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st, const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
     ONEDF_DISPATCH_DK(p->d_k, {
         build_records_kernel<DK><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(K, perm, f->recs, N, total);
     });
+    tr.mark(1, st);
     FwdArgs a;
     a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.qcode = qcode; a.scode = scode; a.recs = f->recs;
     a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.O = O; a.idx = idx; a.Z = Z;
@@ -311,6 +312,7 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
     else if (p->k <= 128) { ONEDF_FWD_KC(128) }
     else { ONEDF_FWD_KC(256) }
 #undef ONEDF_FWD_KC
+    tr.mark(2, st);
     return cudaGetLastError();
 }
 

@@ -10,6 +10,15 @@
 
 namespace onedf {
 
+// Optional stage events (onedf_*_traced): record events[s] after stage s.
+struct Trace {
+    void* const* ev = nullptr;
+    int n = 0;
+    void mark(int s, cudaStream_t st) const {
+        if (ev && s < n && ev[s]) cudaEventRecord((cudaEvent_t)ev[s], st);
+    }
+};
+
 // Longest run the shared-memory segmented sort handles (keys + ping-pong in smem).
 constexpr int64_t SEG_SORT_MAX = 8192;
 
@@ -57,7 +66,7 @@ struct FwdBufs {
 void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f);
 cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                        const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
-                       float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st);
+                       float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st, const Trace& tr);
 
 // bwd.cu
 struct BwdBufs {
@@ -70,6 +79,6 @@ void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b);
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                        const float* O, const float* dO, const int32_t* idx, const float* Z, float* dQ, float* dK,
                        float* dV, double* d_eps, const MeanBufs* m, BwdBufs* b, TransposeBufs* t, void* ws,
-                       cudaStream_t st);
+                       cudaStream_t st, const Trace& tr);
 
 }  // namespace onedf

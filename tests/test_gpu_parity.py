@@ -202,7 +202,7 @@ def test_determinism_bitwise():
     a = gpu_run(kw, x)
     b = gpu_run(kw, x)
     for n in a:
-        assert np.array_equal(np.asarray(a[n]).view(np.uint8), np.asarray(b[n]).view(np.uint8)), n
+        assert np.array_equal(np.atleast_1d(a[n]).view(np.uint8), np.atleast_1d(b[n]).view(np.uint8)), n
 
 
 def test_nonfinite_and_bad_eps_flags():
@@ -226,7 +226,12 @@ def test_nonfinite_and_bad_eps_flags():
     sc, pm = onedf.sort(p, kc, ws=ws)
     V = torch.from_numpy(x["V"]).to(dev)
     onedf.topk_attn_fwd(p, Q, K, V, torch.tensor(0.0, device=dev), qc, sc, pm, ws=ws)
+    ptr, _ = ws.get(0)        # the fwd call may have grown (re-allocated) the workspace
     assert onedf.check_device_status(ptr) == onedf.abi.ERR_NONFINITE
+    onedf.topk_attn_fwd(p, Q, K, V, torch.tensor(float("nan"), device=dev), qc, sc, pm, ws=ws)
+    assert onedf.check_device_status(ptr) == onedf.abi.ERR_NONFINITE
+    onedf.topk_attn_fwd(p, Q, K, V, torch.tensor(0.5, device=dev), qc, sc, pm, ws=ws)
+    assert onedf.check_device_status(ptr) == onedf.OK
 
 
 def test_autograd_function_and_host_step():
