@@ -40,8 +40,7 @@ def alg_bytes(cfg) -> dict:
     s_k, s_v = 4 * dk, 4 * dv
     if cfg.causal:
         M = cfg.chunk
-        m = [i // M for i in range(0, N, 1)]
-        lens = [min(M, N - c * M) for c in range((N + M - 1) // M)]
+        lens =[min(M, N - c * M) for c in range((N + M - 1) // M)]
         # sum over queries of admissible runs / candidates / selected
         sum_m = sum_c = sum_kappa = 0
         prefix_w = [0]
@@ -54,7 +53,6 @@ def alg_bytes(cfg) -> dict:
             sum_m += nq * c
             sum_c += nq * prefix_w[c]
             sum_kappa += nq * min(k, prefix_len[c])
-        del m
         Lbits = max(1, (M).bit_length())
     else:
         sum_m = N
@@ -62,8 +60,7 @@ def alg_bytes(cfg) -> dict:
         sum_kappa = N * min(k, N)
         Lbits = max(1, N.bit_length())
     BH = cfg.BH
-    enc = 4 * N * s_k / 2 + 16 * N                      # fit+encode reads (2 passes over Q,K) + codes
-    enc = 4 * N * s_k + 16 * N
+    enc = 4 * N * s_k + 16 * N                          # fit + encode reads of Q, K; codes written
     srt = 20 * N
     means = 2 * N * (s_k + s_v)
     fwd = N * (8 + s_k) + 8 * Lbits * sum_m + (s_k + 4) * sum_c + s_v * sum_kappa + N * (s_k + s_v) \
@@ -168,16 +165,13 @@ def _dist_env():
     return world, rank, local
 
 
-def _rank_cfg(cfg, rank):
-    """Each rank's own batch: the config's B x H slices, seeded by global slice id."""
-    return cfg
-
-
 def _make_rank_inputs(cfg, rank):
+    """Each rank's own batch (weak scaling): the config's B x H slices, seeded by global slice id."""
     import numpy as np
 
     import synth
-    bhs = range(rank * cfg.BH, (rank + 1) * cfg.BH)
+    from paper_2501_14577_b200.dist import weak_slices
+    bhs = weak_slices(cfg.BH, rank)
     x = synth.make_inputs(cfg, bh_range=bhs)
     return {n: np.ascontiguousarray(v.reshape(cfg.B, cfg.H, *v.shape[2:])) for n, v in x.items()}
 
@@ -252,6 +246,7 @@ def run_gpu(args, cfg, world, rank, local):
         dist.barrier()
     import paper_2501_14577_b200 as onedf
     from paper_2501_14577_b200 import abi
+    from paper_2501_14577_b200 import dist as odist
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -296,12 +291,7 @@ def run_gpu(args, cfg, world, rank, local):
         abi.onedf_topk_attn_bwd_traced(p, t["Q"], t["K"], t["V"], eps, O, t["dO"], idx, Z, dQ, dK, dV, d_eps, ws,
                                        need, ev[6:12], stream)
         if world > 1:
-            parts = [torch.empty((), dtype=torch.float64, device=dev) for _ in range(world)]
-            dist.all_gather(parts, d_eps)
-            total = parts[0].clone()
-            for q in parts[1:]:
-                total += q            # fixed rank order: deterministic
-            d_eps.copy_(total)
+            odist.combine_d_eps(d_eps)      # one f64 per rank, rank-ordered sum (D20)
         ev[12].record(stream)
 
     stage_names = ["encode", "sort", "fwd_means", "fwd_records", "fwd_topk", "bwd_means", "bwd_query",
