@@ -288,8 +288,8 @@ def run_gpu(args, cfg, world, rank, local):
         ev[2].record(stream)
         abi.onedf_topk_attn_fwd_traced(p, t["Q"], t["K"], t["V"], eps, qcode, scode, perm, O, idx, Z, ws, need,
                                        ev[3:6], stream)
-        abi.onedf_topk_attn_bwd_traced(p, t["Q"], t["K"], t["V"], eps, O, t["dO"], idx, Z, dQ, dK, dV, d_eps, ws,
-                                       need, ev[6:12], stream)
+        abi.onedf_topk_attn_bwd_traced(p, t["Q"], t["K"], t["V"], eps, O, t["dO"], idx, Z, qcode, perm, dQ, dK, dV,
+                                       d_eps, ws, need, ev[6:12], stream)
         if world > 1:
             odist.combine_d_eps(d_eps)      # one f64 per rank, rank-ordered sum (D20)
         ev[12].record(stream)

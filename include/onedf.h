@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define ONEDF_VERSION 100
+#define ONEDF_VERSION 200
 
 typedef struct CUstream_st* onedf_stream_t;   /* == cudaStream_t */
 
@@ -139,11 +139,17 @@ onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const f
  * eps (D20).  dK/dV accumulate through a stable sort of (j, slot) pairs and
  * fixed-order f64 segment sums -- no float atomics.
  *   O, Z, idx  the forward's outputs for the same inputs.
+ *   qcode      nullable scheduling hint: the forward's query codes.  When
+ *              given, queries are visited in Morton order per chunk (better
+ *              L1 reuse of the gathered V rows); outputs are bitwise the same.
+ *   perm       nullable scheduling hint: onedf_sort's perm.  When given, keys
+ *              are visited in sorted-run order; outputs are bitwise the same.
  *   dQ, dK, dV overwritten (f32); d_eps device DOUBLE scalar, overwritten with
  *   the sum over all (b,h,i). */
 onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K,
                                  const float* V, const float* eps, const float* O,
                                  const float* dO, const int32_t* idx, const float* Z,
+                                 const uint64_t* qcode, const int32_t* perm,
                                  float* dQ, float* dK, float* dV, double* d_eps,
                                  void* ws, size_t ws_bytes, onedf_stream_t stream);
 
@@ -162,6 +168,7 @@ onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, 
 onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K,
                                         const float* V, const float* eps, const float* O,
                                         const float* dO, const int32_t* idx, const float* Z,
+                                        const uint64_t* qcode, const int32_t* perm,
                                         float* dQ, float* dK, float* dV, double* d_eps,
                                         void* ws, size_t ws_bytes, void* const* events, int n_events,
                                         onedf_stream_t stream);

@@ -13,7 +13,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libonedf.so")
+# ONEDF_LIB: load an alternative build of the same library (tools/ variant timing only)
+LIB_PATH = os.environ.get("ONEDF_LIB") or os.path.join(_PKG, "libonedf.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NONFINITE, ERR_WORKSPACE = range(6)
 OP_ENCODE, OP_SORT, OP_FWD, OP_BWD, OP_STEP_HOST = range(5)
@@ -57,10 +58,10 @@ def _load():
         "onedf_encode": (i32, [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_sort": (i32, [P, vp, vp, vp, vp, sz, vp]),
         "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32, vp]),
-        "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32,
-                                             vp]),
+        "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp,
+                                             i32, vp]),
         "onedf_topk_attn_step_host": (i32, [P, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_check_device_status": (i32, [vp, vp]),
         "onedf_status_string": (ctypes.c_char_p, [i32]),
@@ -137,9 +138,11 @@ def onedf_topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, ws_b
            "onedf_topk_attn_fwd")
 
 
-def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, ws_bytes, stream=None):
+def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, ws_bytes, stream=None):
+    """qcode/perm are nullable scheduling hints (None -> natural order); outputs do not depend on them."""
     _check(_lib.onedf_topk_attn_bwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx), _p(Z),
-                                    _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes, _stream(stream)),
+                                    _p(qcode), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes,
+                                    _stream(stream)),
            "onedf_topk_attn_bwd")
 
 
@@ -155,12 +158,12 @@ def onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, w
                                            _stream(stream)), "onedf_topk_attn_fwd_traced")
 
 
-def onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, ws_bytes, events,
-                               stream=None):
+def onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, ws_bytes,
+                               events, stream=None):
     arr, n = _events(events)
     _check(_lib.onedf_topk_attn_bwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx),
-                                           _p(Z), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes, arr, n,
-                                           _stream(stream)), "onedf_topk_attn_bwd_traced")
+                                           _p(Z), _p(qcode), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws),
+                                           ws_bytes, arr, n, _stream(stream)), "onedf_topk_attn_bwd_traced")
 
 
 def onedf_topk_attn_step_host(p, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_h, dV_h, d_eps_h, ws, ws_bytes,

@@ -86,15 +86,21 @@ def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | 
     return O, idx, Z
 
 
-def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None):
-    """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor])."""
+def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None, qcode=None, perm=None):
+    """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor]).
+
+    qcode/perm (optional) only choose the visiting order (Morton schedule); the
+    outputs are bitwise identical with or without them."""
     Q, K, V, eps, O, dO = _dev(Q), _dev(K), _dev(V), _dev(eps), _dev(O), _dev(dO)
     dQ = torch.empty_like(Q)
     dK = torch.empty_like(K)
     dV = torch.empty_like(V)
     d_eps = torch.empty((), dtype=torch.float64, device=Q.device)
     ptr, n = _ws(p, abi.OP_BWD, ws)
-    abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32), _dev(Z), dQ, dK, dV, d_eps, ptr, n)
+    qcode = None if qcode is None else _dev(qcode, torch.int64)
+    perm = None if perm is None else _dev(perm, torch.int32)
+    abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32), _dev(Z), qcode, perm, dQ, dK, dV, d_eps,
+                            ptr, n)
     return dQ, dK, dV, d_eps
 
 
@@ -111,15 +117,16 @@ class ZetaTopkAttention(torch.autograd.Function):
         qcode, kcode, _ = encode(p, Q, K, ws=ws)
         scode, perm = sort(p, kcode, ws=ws)
         O, idx, Z = topk_attn_fwd(p, Q, K, V, eps.reshape(()), qcode, scode, perm, ws=ws)
-        ctx.save_for_backward(Q, K, V, eps, O, idx, Z)
+        ctx.save_for_backward(Q, K, V, eps, O, idx, Z, qcode, perm)
         ctx.p = p
         ctx.mark_non_differentiable(idx)
         return O, idx
 
     @staticmethod
     def backward(ctx, dO, _didx):
-        Q, K, V, eps, O, idx, Z = ctx.saved_tensors
-        dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps.reshape(()), O, dO.contiguous(), idx, Z)
+        Q, K, V, eps, O, idx, Z, qcode, perm = ctx.saved_tensors
+        dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps.reshape(()), O, dO.contiguous(), idx, Z,
+                                          qcode=qcode, perm=perm)
         return dQ, dK, dV, d_eps.to(eps.dtype).reshape(eps.shape), None
 
 

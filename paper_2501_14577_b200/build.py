@@ -33,15 +33,16 @@ def _headers():
     return hs
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, objdir: str = OBJDIR) -> str:
+    """defines/lib/objdir: variant builds for tools/ experiments (the product is the default)."""
+    os.makedirs(objdir, exist_ok=True)
     hdrs = _headers()
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src.replace(".cu", ".o"))
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", o]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((cmd, o))
@@ -57,12 +58,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for log in ex.map(run, jobs):
             if verbose and log:
                 sys.stderr.write(log)
-    objs = [os.path.join(OBJDIR, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart"]
+    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+    if force or jobs or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"]
         subprocess.run(cmd, check=True)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

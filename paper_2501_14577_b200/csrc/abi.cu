@@ -144,16 +144,16 @@ static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* 
     return finish(e);
 }
 static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                           const float* O, const float* dO, const int32_t* idx, const float* Z, float* dQ, float* dK,
-                           float* dV, double* d_eps, void* ws, cudaStream_t st, bool zero,
-                           const Trace& tr = Trace()) {
+                           const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
+                           const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, void* ws,
+                           cudaStream_t st, bool zero, const Trace& tr = Trace()) {
     if (zero && cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
     BwdLayout L = bwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
     tr.mark(0, st);
     if (e == cudaSuccess)
-        e = launch_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st, tr);
+        e = launch_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st, tr);
     return finish(e);
 }
 
@@ -209,14 +209,14 @@ onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const f
 
 onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V,
                                  const float* eps, const float* O, const float* dO, const int32_t* idx,
-                                 const float* Z, float* dQ, float* dK, float* dV, double* d_eps, void* ws,
-                                 size_t ws_bytes, onedf_stream_t stream) {
+                                 const float* Z, const uint64_t* qcode, const int32_t* perm, float* dQ, float* dK,
+                                 float* dV, double* d_eps, void* ws, size_t ws_bytes, onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_BWD);
     if (s != ONEDF_OK) return s;
     if (!Q || !K || !V || !eps || !O || !dO || !idx || !Z || !dQ || !dK || !dV || !d_eps)
         return ONEDF_ERR_INVALID_ARG;
     if ((((uintptr_t)V) | ((uintptr_t)dO) | ((uintptr_t)dV)) & 15) return ONEDF_ERR_INVALID_ARG;
-    return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true);
+    return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true);
 }
 
 onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K, const float* V,
@@ -235,8 +235,9 @@ onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, 
 
 onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K, const float* V,
                                         const float* eps, const float* O, const float* dO, const int32_t* idx,
-                                        const float* Z, float* dQ, float* dK, float* dV, double* d_eps, void* ws,
-                                        size_t ws_bytes, void* const* events, int n_events, onedf_stream_t stream) {
+                                        const float* Z, const uint64_t* qcode, const int32_t* perm, float* dQ,
+                                        float* dK, float* dV, double* d_eps, void* ws, size_t ws_bytes,
+                                        void* const* events, int n_events, onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_BWD);
     if (s != ONEDF_OK) return s;
     if (!Q || !K || !V || !eps || !O || !dO || !idx || !Z || !dQ || !dK || !dV || !d_eps)
@@ -245,7 +246,8 @@ onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, 
     Trace tr;
     tr.ev = events;
     tr.n = n_events;
-    return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true, tr);
+    return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true,
+                  tr);
 }
 
 onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h, const float* V_h,
@@ -276,7 +278,8 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
     if ((s = do_sort(p, L.kcode, L.scode, L.perm, st)) != ONEDF_OK) return s;
     if ((s = do_fwd(p, L.Q, L.K, L.V, L.eps, L.qcode, L.scode, L.perm, L.O, L.idx, L.Z, sub, st, false)) != ONEDF_OK)
         return s;
-    if ((s = do_bwd(p, L.Q, L.K, L.V, L.eps, L.O, L.dO, L.idx, L.Z, L.dQ, L.dK, L.dV, L.d_eps, sub, st, false)) !=
+    if ((s = do_bwd(p, L.Q, L.K, L.V, L.eps, L.O, L.dO, L.idx, L.Z, L.qcode, L.perm, L.dQ, L.dK, L.dV, L.d_eps, sub,
+                    st, false)) !=
         ONEDF_OK)
         return s;
     e = cudaMemcpyAsync(ws, sub, 4, cudaMemcpyDeviceToDevice, st);   // surface device flags in the caller's header

@@ -12,12 +12,21 @@
 //   dk_j  = sum_{i: j in I_i} w_ij (q_i - k_j)
 // plus the mean slot as one more slot (its A, w go to the A11 scan).
 //
-// K7: one warp per query; a LANE per slot (each lane reads a whole v_j row
-// as float4 bursts and dots it with dO_i broadcast from shared memory), so
-// the 64-wide dot products need no shuffles; f64 arithmetic throughout.
-// K9: one warp per key j walks its CSR segment of (query, slot) pairs in
-// ascending slot order (the stable transpose fixes the order), with f64
-// accumulators: a deterministic segment reduction, no float atomics.
+// K7: one warp per query, queries visited in the Morton schedule (optional;
+// see fwd.cu) so neighbouring warps gather overlapping V rows through L1.
+// P lanes read one v_j row (P float4 chunks = one coalesced 256-B row at
+// d_v = 64), each lane dots its chunk with its slice of dO_i (f64, exact f32
+// products); after T steps every lane holds T partial dots of T different
+// rows, and a butterfly reduce-scatter (log2 P xor-shuffle levels, halving
+// the live values each level) leaves each row's full dot product on one
+// lane.  That lane forms g, A, w for its slot, writes the (A, w) pair the
+// key side consumes, and accumulates dq and deps in f64.
+// K9: one warp per key j (keys visited in sorted-run order when perm is
+// given) walks its CSR segment of (query, slot) pairs in ascending slot order
+// (fixed by the stable transpose): lanes load 32 entries at a time
+// (coalesced), lane groups of P gather the dO_i rows, f64 accumulators, a
+// fixed shuffle tree at the end -- a deterministic segment reduction, no
+// float atomics.  Every per-row result is independent of the visiting order.
 #include "common.cuh"
 #include "internal.h"
 
@@ -31,237 +40,382 @@ void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b) {
     const int64_t BH = p->B * p->H, total = BH * p->N;
     b->coeff = c->take<float2>((size_t)(total * p->k));
     b->muco = c->take<float2>((size_t)total);
-    b->eps_blocks = (int)((total + BWD_WARPS - 1) / BWD_WARPS);
-    b->eps_part = c->take<double>((size_t)b->eps_blocks);
+    b->eps_q = c->take<double>((size_t)total);
+    b->eps_part = c->take<double>((size_t)EPS_PARTS);
+    b->qorder = c->take<int32_t>((size_t)total);
 }
 
 struct BwdArgs {
     const float* Q; const float* K; const float* V; const float* eps;
     const float* O; const float* dO; const int32_t* idx; const float* Z;
-    const float* Kbar; const float* Vbar;
-    float* dQ; float2* coeff; float2* muco; double* eps_part;
+    const float* Kbar; const float* Vbar; const int32_t* qorder;
+    float* dQ; float2* coeff; float2* muco; double* eps_q;
     int64_t N, total;
     int k, dv, causal, mean_slot;
     void* ws;
 };
 
-template <int DK>
-__global__ void __launch_bounds__(BWD_THREADS) bwd_query_kernel(const BwdArgs a) {
-    __shared__ __align__(16) float s_dO[BWD_WARPS][MAX_DV];
-    __shared__ double s_eps[BWD_WARPS];
-    const int warp = threadIdx.x / 32, lane = lane_id();
-    const int64_t gq = (int64_t)blockIdx.x * BWD_WARPS + warp;
-    const int64_t N = a.N;
-    double deps_w = 0.0;
-    if (gq < a.total) {
-        const int64_t bh = gq / N, i = gq % N;
-        const float e = __ldg(a.eps);
-        if (gq == 0 && lane == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
-        const double ed = (double)e;
-        const int dv = a.dv, k = a.k;
-        float q[DK];
+// Butterfly reduce-scatter of T partials over the P lanes of a lane group:
+// afterwards the lane with in-group index l holds the full sum of partial
+// t = l >> (log2 P - log2 T) in v[0].
+template <int P, int T>
+__device__ __forceinline__ void reduce_scatter(double (&v)[T]) {
+    int live = T;
 #pragma unroll
-        for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
-        // dO_i to shared memory; c_i = dO_i . o_i (fixed-order warp tree)
-        float* sdo = s_dO[warp];
-        double cpart = 0.0;
-        for (int d = lane; d < dv; d += 32) {
-            const float g = __ldg(a.dO + gq * dv + d);
-            sdo[d] = g;
-            cpart = fma((double)g, (double)__ldg(a.O + gq * dv + d), cpart);
-        }
-        const double c = warp_sum(cpart);
-        __syncwarp();
-        const double Zi = (double)__ldg(a.Z + gq);
-        const int64_t mrow = a.causal ? i : 0;
-        double dq[DK];
+    for (int s = P / 2; s >= 1; s >>= 1) {
+        if (live > 1) {
+            const int half = live / 2;
+            const bool upper = (lane_id() & s) != 0;
 #pragma unroll
-        for (int d = 0; d < DK; ++d) dq[d] = 0.0;
-        double deps = 0.0;
-        float2* crow = a.coeff + gq * k;
-        if (Zi > 0.0) {
-            const double invZ = 1.0 / Zi;
-            const float* Vb = a.V + bh * N * (int64_t)dv;
-            for (int r = lane; r < k; r += 32) {
-                const int32_t j = __ldg(a.idx + gq * k + r);
-                if (j < 0) { crow[r] = make_float2(0.f, 0.f); continue; }
-                float kj[DK];
-#pragma unroll
-                for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + j) * DK + d);
-                const double delta = dist64<DK>(q, kj) + ed;
-                const double A = (1.0 / delta) * invZ;
-                const float4* vr = reinterpret_cast<const float4*>(Vb + (int64_t)j * dv);
-                const float4* dr = reinterpret_cast<const float4*>(sdo);
-                double dot = 0.0;
-                for (int v = 0; v < dv / 4; ++v) {
-                    const float4 x = __ldg(vr + v);
-                    const float4 y = dr[v];
-                    dot = fma((double)x.x, (double)y.x, dot);
-                    dot = fma((double)x.y, (double)y.y, dot);
-                    dot = fma((double)x.z, (double)y.z, dot);
-                    dot = fma((double)x.w, (double)y.w, dot);
+            for (int m = 0; m < T / 2; ++m) {
+                if (m < half) {
+                    const double send = upper ? v[m] : v[m + half];
+                    const double keep = upper ? v[m + half] : v[m];
+                    v[m] = keep + __shfl_xor_sync(FULL, send, s);
                 }
-                const double g = (dot - c) * invZ;
-                const double inv_d2 = 1.0 / (delta * delta);
-                const double w = 2.0 * g * inv_d2;
-                crow[r] = make_float2((float)A, (float)w);
-#pragma unroll
-                for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] - (double)kj[d]);
-                deps -= g * inv_d2;
             }
-            if (a.mean_slot) {
-                // mean slot: dims split over lanes for the dot product
-                double dpart = 0.0;
-                const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)dv;
-                for (int d = lane; d < dv; d += 32) dpart = fma((double)sdo[d], (double)__ldg(vbar + d), dpart);
-                const double dot = warp_sum(dpart);
-                float kb[DK];
-#pragma unroll
-                for (int d = 0; d < DK; ++d) kb[d] = __ldg(a.Kbar + (bh * (a.causal ? N : 1) + mrow) * DK + d);
-                const double delta = dist64<DK>(q, kb) + ed;
-                const double A = (1.0 / delta) * invZ;
-                const double g = (dot - c) * invZ;
-                const double inv_d2 = 1.0 / (delta * delta);
-                const double w = 2.0 * g * inv_d2;
-                if (lane == 0) {
-#pragma unroll
-                    for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] - (double)kb[d]);
-                    deps -= g * inv_d2;
-                    a.muco[gq] = make_float2((float)A, (float)w);
-                }
-            } else if (lane == 0) {
-                a.muco[gq] = make_float2(0.f, 0.f);
-            }
+            live = half;
         } else {
-            for (int r = lane; r < k; r += 32) crow[r] = make_float2(0.f, 0.f);
-            if (lane == 0) a.muco[gq] = make_float2(0.f, 0.f);
+            v[0] += __shfl_xor_sync(FULL, v[0], s);
+        }
+    }
+}
+
+template <int DK, int P>
+__global__ void __launch_bounds__(BWD_THREADS) bwd_query_kernel(const BwdArgs a) {
+    constexpr int G = 32 / P;                    // rows per step
+    constexpr int T = P < 16 ? P : 16;           // steps per block (live partials per lane)
+    constexpr int RB = T * G;                    // rows per block
+    constexpr int LOGP = P == 32 ? 5 : P == 16 ? 4 : P == 8 ? 3 : P == 4 ? 2 : P == 2 ? 1 : 0;
+    constexpr int LOGT = T == 16 ? 4 : T == 8 ? 3 : T == 4 ? 2 : T == 2 ? 1 : 0;
+    const int warp = threadIdx.x / 32, lane = lane_id();
+    const int64_t slot = (int64_t)blockIdx.x * BWD_WARPS + warp;
+    if (slot >= a.total) return;
+    const int64_t N = a.N;
+    const int64_t bh = slot / N;
+    const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + slot) : slot % N;
+    const int64_t gq = bh * N + i;
+    const float e = __ldg(a.eps);
+    if (slot == 0 && lane == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
+    const double ed = (double)e;
+    const int dv = a.dv, k = a.k, nch = dv / 4;
+    const int grp = lane / P, l = lane % P;
+    float q[DK];
+#pragma unroll
+    for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
+
+    // this lane's dO chunks (ch = l, l + P) and c_i = dO_i . o_i (fixed-order tree)
+    float4 g4[2];
+    double cpart = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int ch = l + h * P;
+        g4[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ch < nch) {
+            g4[h] = __ldg(reinterpret_cast<const float4*>(a.dO + gq * dv) + ch);
+            if (grp == 0) {
+                const float4 o4 = __ldg(reinterpret_cast<const float4*>(a.O + gq * dv) + ch);
+                cpart = fma((double)g4[h].x, (double)o4.x, cpart);
+                cpart = fma((double)g4[h].y, (double)o4.y, cpart);
+                cpart = fma((double)g4[h].z, (double)o4.z, cpart);
+                cpart = fma((double)g4[h].w, (double)o4.w, cpart);
+            }
+        }
+    }
+    const double c = warp_sum(cpart);
+    const double Zi = (double)__ldg(a.Z + gq);
+    const double invZ = Zi > 0.0 ? 1.0 / Zi : 0.0;
+    const int64_t mrow = a.causal ? i : 0;
+    double dq[DK];
+#pragma unroll
+    for (int d = 0; d < DK; ++d) dq[d] = 0.0;
+    double deps = 0.0;
+    const float* Vb = a.V + bh * N * (int64_t)dv;
+    const int32_t* irow = a.idx + gq * k;
+    float2* crow = a.coeff + gq * k;
+
+    for (int e0 = 0; e0 < k; e0 += RB) {
+        double part[T];
+        int jt[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int row = e0 + t * G + grp;
+            jt[t] = (Zi > 0.0 && row < k) ? __ldg(irow + row) : -1;
         }
 #pragma unroll
-        for (int d = 0; d < DK; ++d) dq[d] = warp_sum(dq[d]);
-        deps = warp_sum(deps);
-        if (lane < DK) {
-            double v = 0.0;
+        for (int t = 0; t < T; ++t) {
+            part[t] = 0.0;
+            if (jt[t] >= 0) {
+                const float4* vr = reinterpret_cast<const float4*>(Vb + (int64_t)jt[t] * dv);
 #pragma unroll
-            for (int d = 0; d < DK; ++d) v = (lane == d) ? dq[d] : v;
-            a.dQ[gq * DK + lane] = (float)v;
+                for (int h = 0; h < 2; ++h) {
+                    const int ch = l + h * P;
+                    if (ch < nch) {
+                        const float4 x = __ldg(vr + ch);
+                        part[t] = fma((double)x.x, (double)g4[h].x, part[t]);
+                        part[t] = fma((double)x.y, (double)g4[h].y, part[t]);
+                        part[t] = fma((double)x.z, (double)g4[h].z, part[t]);
+                        part[t] = fma((double)x.w, (double)g4[h].w, part[t]);
+                    }
+                }
+            }
         }
-        deps_w = deps;
+        reduce_scatter<P, T>(part);
+        // owner of row t = l >> (LOGP - LOGT); one owner per (t, grp)
+        if ((l & ((1 << (LOGP - LOGT)) - 1)) == 0) {
+            const int t = l >> (LOGP - LOGT);
+            const int row = e0 + t * G + grp;
+            if (row < k) {
+                const int32_t j = Zi > 0.0 ? __ldg(irow + row) : -1;
+                if (j < 0) {
+                    crow[row] = make_float2(0.f, 0.f);
+                } else {
+                    float kj[DK];
+#pragma unroll
+                    for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + j) * DK + d);
+                    const double delta = dist64<DK>(q, kj) + ed;
+                    const double A = (1.0 / delta) * invZ;
+                    const double g = (part[0] - c) * invZ;
+                    const double inv_d2 = 1.0 / (delta * delta);
+                    const double w = 2.0 * g * inv_d2;
+                    crow[row] = make_float2((float)A, (float)w);
+#pragma unroll
+                    for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] - (double)kj[d]);
+                    deps -= g * inv_d2;
+                }
+            }
+        }
     }
-    if (lane == 0) s_eps[warp] = deps_w;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < BWD_WARPS; ++w) s += s_eps[w];
-        a.eps_part[blockIdx.x] = s;
+    if (a.mean_slot && Zi > 0.0) {
+        double dpart = 0.0;
+        const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)dv;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int ch = l + h * P;
+            if (grp == 0 && ch < nch) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(vbar) + ch);
+                dpart = fma((double)g4[h].x, (double)x.x, dpart);
+                dpart = fma((double)g4[h].y, (double)x.y, dpart);
+                dpart = fma((double)g4[h].z, (double)x.z, dpart);
+                dpart = fma((double)g4[h].w, (double)x.w, dpart);
+            }
+        }
+        const double dot = warp_sum(dpart);
+        float kb[DK];
+#pragma unroll
+        for (int d = 0; d < DK; ++d) kb[d] = __ldg(a.Kbar + (bh * (a.causal ? N : 1) + mrow) * DK + d);
+        const double delta = dist64<DK>(q, kb) + ed;
+        const double A = (1.0 / delta) * invZ;
+        const double g = (dot - c) * invZ;
+        const double inv_d2 = 1.0 / (delta * delta);
+        const double w = 2.0 * g * inv_d2;
+        if (lane == 0) {
+#pragma unroll
+            for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] - (double)kb[d]);
+            deps -= g * inv_d2;
+            a.muco[gq] = make_float2((float)A, (float)w);
+        }
+    } else if (lane == 0) {
+        a.muco[gq] = make_float2(0.f, 0.f);
     }
+#pragma unroll
+    for (int d = 0; d < DK; ++d) dq[d] = warp_sum(dq[d]);
+    deps = warp_sum(deps);
+    if (lane < DK) {
+        double v = 0.0;
+#pragma unroll
+        for (int d = 0; d < DK; ++d) v = (lane == d) ? dq[d] : v;
+        a.dQ[gq * DK + lane] = (float)v;
+    }
+    if (lane == 0) a.eps_q[gq] = deps;
 }
 
 struct KeyArgs {
     const float* Q; const float* K; const float* dO; const float2* coeff;
-    const uint32_t* slots; const int32_t* offsets;
+    const uint32_t* slots; const int32_t* offsets; const int32_t* korder;
     float* dK; float* dV;
     int64_t N, L, total;
     int k, dv;
 };
 
-template <int DK>
+template <int DK, int P>
 __global__ void __launch_bounds__(BWD_THREADS) bwd_key_kernel(const KeyArgs a) {
+    constexpr int G = 32 / P;
+    constexpr int U = 4;                          // entries per group in flight
     const int warp = threadIdx.x / 32, lane = lane_id();
-    const int64_t gk = (int64_t)blockIdx.x * BWD_WARPS + warp;
-    if (gk >= a.total) return;
-    const int64_t N = a.N, bh = gk / N, j = gk % N;
+    const int64_t slot = (int64_t)blockIdx.x * BWD_WARPS + warp;
+    if (slot >= a.total) return;
+    const int64_t N = a.N, bh = slot / N;
+    const int64_t j = a.korder ? (int64_t)__ldg(a.korder + slot) : slot % N;
+    const int64_t gk = bh * N + j;
     const int32_t* off = a.offsets + bh * (N + 1);
-    const int32_t s0 = off[j], s1 = off[j + 1];
+    const int32_t s0 = __ldg(off + j), s1 = __ldg(off + j + 1);
     const uint32_t* sl = a.slots + bh * a.L;
     const float2* cf = a.coeff + bh * a.L;
-    const int dv = a.dv, k = a.k;
-    const int nch = dv / 4;
-    int P = 1;
-    while (P < nch && P < 32) P <<= 1;
-    const int G = 32 / P, grp = lane / P, ch_l = lane % P;
+    const int dv = a.dv, k = a.k, nch = dv / 4;
+    const int grp = lane / P, l = lane % P;
     float kj[DK];
 #pragma unroll
     for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + gk * DK + d);
     double dk[DK];
 #pragma unroll
     for (int d = 0; d < DK; ++d) dk[d] = 0.0;
+    double acc[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[h][c] = 0.0;
     const float* dOb = a.dO + bh * N * (int64_t)dv;
     const float* Qb = a.Q + bh * N * DK;
-    float* dvrow = a.dV + gk * (int64_t)dv;
-    for (int ch0 = 0; ch0 < nch; ch0 += P) {
-        const int ch = ch0 + ch_l;
-        const bool act = ch < nch;
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-        for (int32_t s = s0 + grp; s < s1; s += G) {
-            const uint32_t slot = __ldg(sl + s);
-            const int64_t iq = slot / (uint32_t)k;
-            const float2 aw = __ldg(cf + slot);
-            if (act) {
-                const float4 g = __ldg(reinterpret_cast<const float4*>(dOb + iq * dv) + ch);
-                const double A = (double)aw.x;
-                acc0 = fma(A, (double)g.x, acc0);
-                acc1 = fma(A, (double)g.y, acc1);
-                acc2 = fma(A, (double)g.z, acc2);
-                acc3 = fma(A, (double)g.w, acc3);
-            }
-            if (ch0 == 0 && ch_l == 0) {
+
+    for (int32_t b0 = s0; b0 < s1; b0 += 32) {
+        // lane-parallel entry loads (coalesced slots, gathered (A, w) and q_i)
+        const int32_t s = b0 + lane;
+        int iq = 0;
+        float A = 0.f;
+        if (s < s1) {
+            const uint32_t sv = __ldg(sl + s);
+            iq = (int)(sv / (uint32_t)k);
+            const float2 aw = __ldg(cf + sv);
+            A = aw.x;
+            // dK: the lane owning the entry, f64, fixed entry -> lane map
 #pragma unroll
-                for (int d = 0; d < DK; ++d) dk[d] += (double)aw.y * ((double)__ldg(Qb + iq * DK + d) - (double)kj[d]);
+            for (int d = 0; d < DK; ++d) dk[d] += (double)aw.y * ((double)__ldg(Qb + (int64_t)iq * DK + d) - (double)kj[d]);
+        }
+        const int n = min(32, s1 - b0);
+        // dV: group g takes entries g, g+G, ... of this chunk, U at a time
+        for (int t0 = 0; t0 < n; t0 += G * U) {
+            float4 x[U][2];
+            double Au[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int src = t0 + u * G + grp;
+                const int iu = __shfl_sync(FULL, iq, src & 31);
+                Au[u] = (double)__shfl_sync(FULL, A, src & 31);
+                const bool ok = src < n;
+                if (!ok) Au[u] = 0.0;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int ch = l + h * P;
+                    x[u][h] = (ok && ch < nch) ? __ldg(reinterpret_cast<const float4*>(dOb + (int64_t)iu * dv) + ch)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    acc[h][0] = fma(Au[u], (double)x[u][h].x, acc[h][0]);
+                    acc[h][1] = fma(Au[u], (double)x[u][h].y, acc[h][1]);
+                    acc[h][2] = fma(Au[u], (double)x[u][h].z, acc[h][2]);
+                    acc[h][3] = fma(Au[u], (double)x[u][h].w, acc[h][3]);
+                }
         }
-        for (int o = P; o < 32; o <<= 1) {
-            acc0 += __shfl_xor_sync(FULL, acc0, o);
-            acc1 += __shfl_xor_sync(FULL, acc1, o);
-            acc2 += __shfl_xor_sync(FULL, acc2, o);
-            acc3 += __shfl_xor_sync(FULL, acc3, o);
-        }
-        if (grp == 0 && act)
-            reinterpret_cast<float4*>(dvrow)[ch] = make_float4((float)acc0, (float)acc1, (float)acc2, (float)acc3);
     }
-    // dK: group leaders (lanes 0, P, 2P, ...) hold partial sums over their slots
 #pragma unroll
-    for (int d = 0; d < DK; ++d)
-        for (int o = P; o < 32; o <<= 1) dk[d] += __shfl_xor_sync(FULL, dk[d], o);
-    if (lane == 0) {
+    for (int o = P; o < 32; o <<= 1)
 #pragma unroll
-        for (int d = 0; d < DK; ++d) a.dK[gk * DK + d] = (float)dk[d];
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[h][c] += __shfl_xor_sync(FULL, acc[h][c], o);
+    if (grp == 0) {
+        float* dvrow = a.dV + gk * (int64_t)dv;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int ch = l + h * P;
+            if (ch < nch)
+                reinterpret_cast<float4*>(dvrow)[ch] =
+                    make_float4((float)acc[h][0], (float)acc[h][1], (float)acc[h][2], (float)acc[h][3]);
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < DK; ++d) dk[d] = warp_sum(dk[d]);
+    if (lane < DK) {
+        double v = 0.0;
+#pragma unroll
+        for (int d = 0; d < DK; ++d) v = (lane == d) ? dk[d] : v;
+        a.dK[gk * DK + lane] = (float)v;
     }
 }
 
-__global__ void eps_reduce_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+// A12: dε = Σ over all (b,h,i) of the per-query partials, in a fixed order:
+// EPS_PARTS contiguous ranges summed by fixed block trees, then one block.
+__global__ void __launch_bounds__(256) eps_partial_kernel(const double* __restrict__ eps_q, int64_t n,
+                                                          double* __restrict__ part) {
     __shared__ double s[256];
+    const int64_t per = (n + EPS_PARTS - 1) / EPS_PARTS;
+    const int64_t a0 = (int64_t)blockIdx.x * per, a1 = min64(n, a0 + per);
     double acc = 0.0;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) acc += part[t];
+    for (int64_t t = a0 + threadIdx.x; t < a1; t += 256) acc += eps_q[t];
     s[threadIdx.x] = acc;
     __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = s[0];
+}
+
+__global__ void __launch_bounds__(256) eps_final_kernel(const double* __restrict__ part, double* __restrict__ out) {
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int t = threadIdx.x; t < EPS_PARTS; t += 256) acc += part[t];
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
         if ((int)threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
         __syncthreads();
     }
     if (threadIdx.x == 0) *out = s[0];
 }
 
+static int lanes_per_row(int dv) {
+    const int nch = dv / 4;
+    int P = 4;
+    while (P < nch && P < 32) P <<= 1;
+    return P;
+}
+
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                       const float* O, const float* dO, const int32_t* idx, const float* Z, float* dQ, float* dK,
-                       float* dV, double* d_eps, const MeanBufs* m, BwdBufs* b, TransposeBufs* t, void* ws,
-                       cudaStream_t st, const Trace& tr) {
+                       const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
+                       const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, const MeanBufs* m,
+                       BwdBufs* b, TransposeBufs* t, void* ws, cudaStream_t st, const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
+    cudaError_t e = cudaSuccess;
+    const int32_t* qorder = nullptr;
+    if (qcode) {
+        e = launch_query_order(p, qcode, b->qorder, st);
+        if (e != cudaSuccess) return e;
+        qorder = b->qorder;
+    }
     BwdArgs a;
     a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.O = O; a.dO = dO; a.idx = idx; a.Z = Z;
-    a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.dQ = dQ; a.coeff = b->coeff; a.muco = b->muco; a.eps_part = b->eps_part;
+    a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.qorder = qorder;
+    a.dQ = dQ; a.coeff = b->coeff; a.muco = b->muco; a.eps_q = b->eps_q;
     a.N = N; a.total = total; a.k = p->k; a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
     a.ws = ws;
-    ONEDF_DISPATCH_DK(p->d_k, { bwd_query_kernel<DK><<<(unsigned)b->eps_blocks, BWD_THREADS, 0, st>>>(a); });
+    const int P = lanes_per_row(p->d_v);
+    const unsigned qgrid = (unsigned)((total + BWD_WARPS - 1) / BWD_WARPS);
+#define ONEDF_BWDQ(PV) ONEDF_DISPATCH_DK(p->d_k, { bwd_query_kernel<DK, PV><<<qgrid, BWD_THREADS, 0, st>>>(a); })
+    if (P == 4) { ONEDF_BWDQ(4) }
+    else if (P == 8) { ONEDF_BWDQ(8) }
+    else if (P == 16) { ONEDF_BWDQ(16) }
+    else { ONEDF_BWDQ(32) }
+#undef ONEDF_BWDQ
     tr.mark(1, st);
-    cudaError_t e = launch_transpose(p, idx, t, st);
+    e = launch_transpose(p, idx, t, st);
     if (e != cudaSuccess) return e;
     tr.mark(2, st);
     KeyArgs ka;
     ka.Q = Q; ka.K = K; ka.dO = dO; ka.coeff = b->coeff; ka.slots = t->slots; ka.offsets = t->offsets;
+    ka.korder = perm;
     ka.dK = dK; ka.dV = dV; ka.N = N; ka.L = N * (int64_t)p->k; ka.total = total; ka.k = p->k; ka.dv = p->d_v;
-    ONEDF_DISPATCH_DK(p->d_k, {
-        bwd_key_kernel<DK><<<(unsigned)((total + BWD_WARPS - 1) / BWD_WARPS), BWD_THREADS, 0, st>>>(ka);
-    });
+#define ONEDF_BWDK(PV) ONEDF_DISPATCH_DK(p->d_k, { bwd_key_kernel<DK, PV><<<qgrid, BWD_THREADS, 0, st>>>(ka); })
+    if (P == 4) { ONEDF_BWDK(4) }
+    else if (P == 8) { ONEDF_BWDK(8) }
+    else if (P == 16) { ONEDF_BWDK(16) }
+    else { ONEDF_BWDK(32) }
+#undef ONEDF_BWDK
     tr.mark(3, st);
     if (p->mean_slot) {
         e = launch_mean_grad_scan(p, Q, dO, reinterpret_cast<const float*>(b->muco), const_cast<MeanBufs*>(m), dK,
@@ -269,7 +423,8 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
         if (e != cudaSuccess) return e;
     }
     tr.mark(4, st);
-    eps_reduce_kernel<<<1, 256, 0, st>>>(b->eps_part, b->eps_blocks, d_eps);
+    eps_partial_kernel<<<EPS_PARTS, 256, 0, st>>>(b->eps_q, total, b->eps_part);
+    eps_final_kernel<<<1, 256, 0, st>>>(b->eps_part, d_eps);
     tr.mark(5, st);
     return cudaGetLastError();
 }

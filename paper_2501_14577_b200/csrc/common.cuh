@@ -62,9 +62,11 @@ __device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int
 // _rn intrinsics forbid FMA contraction (reading D23).
 template <int DK>
 __device__ __forceinline__ float rank_dist32(const float* q, const float* k) {
-    float acc = 0.f;
+    // 0 + t0^2 == t0^2 exactly (t0^2 >= +0), so the chain starts at t0^2
+    const float t0 = __fsub_rn(q[0], k[0]);
+    float acc = __fmul_rn(t0, t0);
 #pragma unroll
-    for (int d = 0; d < DK; ++d) {
+    for (int d = 1; d < DK; ++d) {
         float t = __fsub_rn(q[d], k[d]);
         acc = __fadd_rn(acc, __fmul_rn(t, t));
     }

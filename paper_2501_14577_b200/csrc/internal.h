@@ -34,14 +34,17 @@ cudaError_t launch_encode(const onedf_problem* p, int b, const float* Q, const f
                           cudaStream_t st);
 
 // sort.cu
-cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode, int32_t* perm,
-                            cudaStream_t st);
+cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode /* nullable */,
+                            int32_t* perm, cudaStream_t st);
+cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, int32_t* qorder, cudaStream_t st);
 struct TransposeBufs {
     uint32_t* keys[2];
     uint32_t* vals[2];
-    uint32_t* hist;     // [BH][buckets][tiles]
+    uint32_t* hist;     // [BH][256][tiles] per-tile digit counts -> tile offsets within the digit
+    uint32_t* dtot;     // [BH][256] digit totals of the current pass
+    uint32_t* nvalid;   // [BH] valid (j >= 0) pairs
     int32_t* offsets;   // [BH][N+1]  CSR: slots of key j are sorted[off[j], off[j+1])
-    uint32_t* slots;    // final sorted slot ids (points into keys/vals)
+    uint32_t* slots;    // final sorted slot ids (points into vals)
 };
 void transpose_carve(const onedf_problem* p, Carver* c, TransposeBufs* t);
 cudaError_t launch_transpose(const onedf_problem* p, const int32_t* idx, TransposeBufs* t, cudaStream_t st);
@@ -62,6 +65,7 @@ cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const 
 // fwd.cu
 struct FwdBufs {
     float* recs;        // [BH][N][RecW] sorted key records
+    int32_t* qorder;    // [BH][N] query schedule (per chunk, by qcode)
 };
 void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f);
 cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
@@ -69,16 +73,18 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
                        float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st, const Trace& tr);
 
 // bwd.cu
+constexpr int EPS_PARTS = 1024;   // fixed first-level split of the d_eps reduction
 struct BwdBufs {
     float2* coeff;      // [BH][N][k] (A, w)
     float2* muco;       // [BH][N]    (A_mu, w_mu)
-    double* eps_part;   // [blocks]
-    int eps_blocks;
+    double* eps_q;      // [BH][N]    per-query d_eps contribution
+    double* eps_part;   // [EPS_PARTS]
+    int32_t* qorder;    // [BH][N]    query schedule (when qcode is given)
 };
 void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b);
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                       const float* O, const float* dO, const int32_t* idx, const float* Z, float* dQ, float* dK,
-                       float* dV, double* d_eps, const MeanBufs* m, BwdBufs* b, TransposeBufs* t, void* ws,
-                       cudaStream_t st, const Trace& tr);
+                       const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
+                       const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, const MeanBufs* m,
+                       BwdBufs* b, TransposeBufs* t, void* ws, cudaStream_t st, const Trace& tr);
 
 }  // namespace onedf

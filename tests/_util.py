@@ -26,7 +26,8 @@ def gpu_run(kw: dict, x: dict, eps: float = synth.EPS, bwd: bool = True, lohi=No
     O, idx, Z = onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws)
     out = dict(qcode=qc, kcode=kc, lohi=lohi_out, scode=sc, perm=pm, O=O, idx=idx, Z=Z)
     if bwd:
-        dQ, dK, dV, d_eps = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws)
+        dQ, dK, dV, d_eps = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws,
+                                                qcode=qc, perm=pm)
         out.update(dQ=dQ, dK=dK, dV=dV, d_eps=d_eps)
     torch.cuda.synchronize()
     res = {}

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(onedf):
     for name in _declared_functions():
         assert hasattr(lib, name), name
     assert set(onedf.abi.EXPORTS) == set(_declared_functions())
-    assert onedf.onedf_version() == 100
+    assert onedf.onedf_version() == 200
 
 
 def test_struct_layout_matches_c(onedf, tmp_path):
@@ -91,7 +91,7 @@ def test_calls_check_arguments_before_any_launch(onedf):
     # workspace too small / misaligned / NULL -> ERR_WORKSPACE (checked before the device)
     assert lib.onedf_topk_attn_fwd(ctypes.byref(good), *([256] * 10), 256, 16, None) == onedf.abi.ERR_WORKSPACE
     assert lib.onedf_sort(ctypes.byref(good), 256, 256, 256, 257, 1 << 20, None) == onedf.abi.ERR_WORKSPACE
-    assert lib.onedf_topk_attn_bwd(ctypes.byref(good), *([256] * 12), None, 1 << 40, None) == onedf.abi.ERR_WORKSPACE
+    assert lib.onedf_topk_attn_bwd(ctypes.byref(good), *([256] * 14), None, 1 << 40, None) == onedf.abi.ERR_WORKSPACE
     assert onedf.status_string(onedf.abi.ERR_WORKSPACE).startswith("workspace")
 
 

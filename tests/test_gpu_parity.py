@@ -263,3 +263,29 @@ def test_autograd_function_and_host_step():
     for n in ("O", "dQ", "dK", "dV"):
         assert_close(outs[n].numpy(), ref[n], f"host {n}")
     assert_close(float(d_eps), ref["d_eps"], "host d_eps")
+
+
+@pytest.mark.parametrize("name", ["ar_tokens", "lra_nc"])
+def test_schedule_hints_do_not_change_results(name):
+    """qcode/perm only pick the visiting order of the backward: outputs are bitwise identical."""
+    import torch
+
+    import paper_2501_14577_b200 as onedf
+    cfg = synth.CONFIGS[name]
+    cfg = cfg.with_(B=1, H=2) if cfg.BH > 2 else cfg
+    kw = cfg.problem_kwargs()
+    x = synth.make_inputs(cfg)
+    dev = torch.device("cuda:0")
+    t = {n: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for n, v in x.items()}
+    p = onedf.make_problem(**kw)
+    e = torch.tensor(synth.EPS, dtype=torch.float32, device=dev)
+    ws = onedf.Workspace(dev)
+    qc, kc, _ = onedf.encode(p, t["Q"], t["K"], ws=ws)
+    sc, pm = onedf.sort(p, kc, ws=ws)
+    O, idx, Z = onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws)
+    a = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws, qcode=qc, perm=pm)
+    a = [v.cpu().numpy().copy() for v in a]
+    b = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws)
+    b = [v.cpu().numpy() for v in b]
+    for u, v, n in zip(a, b, ("dQ", "dK", "dV", "d_eps")):
+        assert np.array_equal(np.atleast_1d(u).view(np.uint8), np.atleast_1d(v).view(np.uint8)), n
