@@ -35,6 +35,12 @@ namespace onedf {
 constexpr int BWD_WARPS = 8;
 constexpr int BWD_THREADS = BWD_WARPS * 32;
 constexpr int MAX_DV = 256;
+#ifndef ONEDF_KEY_U
+#define ONEDF_KEY_U 4
+#endif
+#ifndef ONEDF_BWD_MINB
+#define ONEDF_BWD_MINB 4
+#endif
 
 void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b) {
     const int64_t BH = p->B * p->H, total = BH * p->N;
@@ -81,10 +87,10 @@ __device__ __forceinline__ void reduce_scatter(double (&v)[T]) {
     }
 }
 
-template <int DK, int P>
-__global__ void __launch_bounds__(BWD_THREADS) bwd_query_kernel(const BwdArgs a) {
+template <int DK, int P, int CH, int R>
+__global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(const BwdArgs a) {
     constexpr int G = 32 / P;                    // rows per step
-    constexpr int T = P < 16 ? P : 16;           // steps per block (live partials per lane)
+    constexpr int T = P < 8 ? P : 8;             // steps per block (live partials / loads in flight per lane)
     constexpr int RB = T * G;                    // rows per block
     constexpr int LOGP = P == 32 ? 5 : P == 16 ? 4 : P == 8 ? 3 : P == 4 ? 2 : P == 2 ? 1 : 0;
     constexpr int LOGT = T == 16 ? 4 : T == 8 ? 3 : T == 4 ? 2 : T == 2 ? 1 : 0;
@@ -100,15 +106,23 @@ __global__ void __launch_bounds__(BWD_THREADS) bwd_query_kernel(const BwdArgs a)
     const double ed = (double)e;
     const int dv = a.dv, k = a.k, nch = dv / 4;
     const int grp = lane / P, l = lane % P;
+    const double Zi = (double)__ldg(a.Z + gq);
+    // the idx row, lane-parallel (slot e lives on lane e % 32, register e / 32)
+    int jr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e2 = r * 32 + lane;
+        jr[r] = (Zi > 0.0 && e2 < k) ? __ldg(a.idx + gq * k + e2) : -1;
+    }
     float q[DK];
 #pragma unroll
     for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
 
-    // this lane's dO chunks (ch = l, l + P) and c_i = dO_i . o_i (fixed-order tree)
-    float4 g4[2];
+    // this lane's dO chunks (ch = l + h*P, h < CH) and c_i = dO_i . o_i (fixed-order tree)
+    float4 g4[CH];
     double cpart = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < CH; ++h) {
         const int ch = l + h * P;
         g4[h] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (ch < nch) {
@@ -123,7 +137,6 @@ __global__ void __launch_bounds__(BWD_THREADS) bwd_query_kernel(const BwdArgs a)
         }
     }
     const double c = warp_sum(cpart);
-    const double Zi = (double)__ldg(a.Z + gq);
     const double invZ = Zi > 0.0 ? 1.0 / Zi : 0.0;
     const int64_t mrow = a.causal ? i : 0;
     double dq[DK];
@@ -131,48 +144,51 @@ __global__ void __launch_bounds__(BWD_THREADS) bwd_query_kernel(const BwdArgs a)
     for (int d = 0; d < DK; ++d) dq[d] = 0.0;
     double deps = 0.0;
     const float* Vb = a.V + bh * N * (int64_t)dv;
-    const int32_t* irow = a.idx + gq * k;
     float2* crow = a.coeff + gq * k;
+    const int owner_t = l >> (LOGP - LOGT);
+    const bool owner = (l & ((1 << (LOGP - LOGT)) - 1)) == 0;
 
-    for (int e0 = 0; e0 < k; e0 += RB) {
-        double part[T];
-        int jt[T];
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-            const int row = e0 + t * G + grp;
-            jt[t] = (Zi > 0.0 && row < k) ? __ldg(irow + row) : -1;
-        }
+    for (int r = 0; r < R; ++r) {
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-            part[t] = 0.0;
-            if (jt[t] >= 0) {
-                const float4* vr = reinterpret_cast<const float4*>(Vb + (int64_t)jt[t] * dv);
+        for (int h0 = 0; h0 < 32; h0 += RB) {
+            const int e0 = r * 32 + h0;
+            if (e0 >= k) break;                                  // warp-uniform
+            // owner: its row's j and k_j, issued before the V loads
+            const int orow = h0 + owner_t * G + grp;            // lane of the owned slot
+            const int oj = __shfl_sync(FULL, jr[r], orow & 31);
+            float kj[DK];
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+            for (int d = 0; d < DK; ++d) kj[d] = (owner && oj >= 0) ? __ldg(a.K + (bh * N + oj) * DK + d) : 0.f;
+            double part[T];
+            float4 x[T][CH];
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const int j = __shfl_sync(FULL, jr[r], (h0 + t * G + grp) & 31);
+                const float4* vr = reinterpret_cast<const float4*>(Vb + (int64_t)(j < 0 ? 0 : j) * dv);
+#pragma unroll
+                for (int h = 0; h < CH; ++h) {
                     const int ch = l + h * P;
-                    if (ch < nch) {
-                        const float4 x = __ldg(vr + ch);
-                        part[t] = fma((double)x.x, (double)g4[h].x, part[t]);
-                        part[t] = fma((double)x.y, (double)g4[h].y, part[t]);
-                        part[t] = fma((double)x.z, (double)g4[h].z, part[t]);
-                        part[t] = fma((double)x.w, (double)g4[h].w, part[t]);
-                    }
+                    x[t][h] = (j >= 0 && ch < nch) ? __ldg(vr + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
-        }
-        reduce_scatter<P, T>(part);
-        // owner of row t = l >> (LOGP - LOGT); one owner per (t, grp)
-        if ((l & ((1 << (LOGP - LOGT)) - 1)) == 0) {
-            const int t = l >> (LOGP - LOGT);
-            const int row = e0 + t * G + grp;
-            if (row < k) {
-                const int32_t j = Zi > 0.0 ? __ldg(irow + row) : -1;
-                if (j < 0) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                part[t] = 0.0;
+#pragma unroll
+                for (int h = 0; h < CH; ++h) {
+                    part[t] = fma((double)x[t][h].x, (double)g4[h].x, part[t]);
+                    part[t] = fma((double)x[t][h].y, (double)g4[h].y, part[t]);
+                    part[t] = fma((double)x[t][h].z, (double)g4[h].z, part[t]);
+                    part[t] = fma((double)x[t][h].w, (double)g4[h].w, part[t]);
+                }
+            }
+            reduce_scatter<P, T>(part);
+            const int row = e0 + owner_t * G + grp;
+            if (owner && row < k) {
+                if (oj < 0) {
                     crow[row] = make_float2(0.f, 0.f);
                 } else {
-                    float kj[DK];
-#pragma unroll
-                    for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + j) * DK + d);
                     const double delta = dist64<DK>(q, kj) + ed;
                     const double A = (1.0 / delta) * invZ;
                     const double g = (part[0] - c) * invZ;
@@ -190,7 +206,7 @@ __global__ void __launch_bounds__(BWD_THREADS) bwd_query_kernel(const BwdArgs a)
         double dpart = 0.0;
         const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)dv;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < CH; ++h) {
             const int ch = l + h * P;
             if (grp == 0 && ch < nch) {
                 const float4 x = __ldg(reinterpret_cast<const float4*>(vbar) + ch);
@@ -238,10 +254,10 @@ struct KeyArgs {
     int k, dv;
 };
 
-template <int DK, int P>
-__global__ void __launch_bounds__(BWD_THREADS) bwd_key_kernel(const KeyArgs a) {
+template <int DK, int P, int CH>
+__global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(const KeyArgs a) {
     constexpr int G = 32 / P;
-    constexpr int U = 4;                          // entries per group in flight
+    constexpr int U = ONEDF_KEY_U;                // entries per lane group in flight
     const int warp = threadIdx.x / 32, lane = lane_id();
     const int64_t slot = (int64_t)blockIdx.x * BWD_WARPS + warp;
     if (slot >= a.total) return;
@@ -260,42 +276,43 @@ __global__ void __launch_bounds__(BWD_THREADS) bwd_key_kernel(const KeyArgs a) {
     double dk[DK];
 #pragma unroll
     for (int d = 0; d < DK; ++d) dk[d] = 0.0;
-    double acc[2][4];
+    double acc[CH][4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < CH; ++h)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[h][c] = 0.0;
     const float* dOb = a.dO + bh * N * (int64_t)dv;
     const float* Qb = a.Q + bh * N * DK;
 
+    // entry loads of the next 32-entry chunk are issued one chunk ahead
+    uint32_t sv_next = (s0 + lane < s1) ? __ldg(sl + s0 + lane) : 0u;
     for (int32_t b0 = s0; b0 < s1; b0 += 32) {
-        // lane-parallel entry loads (coalesced slots, gathered (A, w) and q_i)
         const int32_t s = b0 + lane;
-        int iq = 0;
-        float A = 0.f;
-        if (s < s1) {
-            const uint32_t sv = __ldg(sl + s);
-            iq = (int)(sv / (uint32_t)k);
-            const float2 aw = __ldg(cf + sv);
-            A = aw.x;
-            // dK: the lane owning the entry, f64, fixed entry -> lane map
+        const bool has = s < s1;
+        const uint32_t sv = sv_next;
+        sv_next = (s + 32 < s1) ? __ldg(sl + s + 32) : 0u;
+        const int iq = (int)(sv / (uint32_t)k);
+        float2 aw = make_float2(0.f, 0.f);
+        float qi[DK];
+        if (has) {
+            aw = __ldg(cf + sv);
 #pragma unroll
-            for (int d = 0; d < DK; ++d) dk[d] += (double)aw.y * ((double)__ldg(Qb + (int64_t)iq * DK + d) - (double)kj[d]);
+            for (int d = 0; d < DK; ++d) qi[d] = __ldg(Qb + (int64_t)iq * DK + d);
         }
         const int n = min(32, s1 - b0);
         // dV: group g takes entries g, g+G, ... of this chunk, U at a time
         for (int t0 = 0; t0 < n; t0 += G * U) {
-            float4 x[U][2];
-            double Au[U];
+            float4 x[U][CH];
+            float Au[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int src = t0 + u * G + grp;
                 const int iu = __shfl_sync(FULL, iq, src & 31);
-                Au[u] = (double)__shfl_sync(FULL, A, src & 31);
+                Au[u] = __shfl_sync(FULL, aw.x, src & 31);
                 const bool ok = src < n;
-                if (!ok) Au[u] = 0.0;
+                if (!ok) Au[u] = 0.f;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < CH; ++h) {
                     const int ch = l + h * P;
                     x[u][h] = (ok && ch < nch) ? __ldg(reinterpret_cast<const float4*>(dOb + (int64_t)iu * dv) + ch)
                                                : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -304,24 +321,30 @@ __global__ void __launch_bounds__(BWD_THREADS) bwd_key_kernel(const KeyArgs a) {
 #pragma unroll
             for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    acc[h][0] = fma(Au[u], (double)x[u][h].x, acc[h][0]);
-                    acc[h][1] = fma(Au[u], (double)x[u][h].y, acc[h][1]);
-                    acc[h][2] = fma(Au[u], (double)x[u][h].z, acc[h][2]);
-                    acc[h][3] = fma(Au[u], (double)x[u][h].w, acc[h][3]);
+                for (int h = 0; h < CH; ++h) {
+                    const double A = (double)Au[u];
+                    acc[h][0] = fma(A, (double)x[u][h].x, acc[h][0]);
+                    acc[h][1] = fma(A, (double)x[u][h].y, acc[h][1]);
+                    acc[h][2] = fma(A, (double)x[u][h].z, acc[h][2]);
+                    acc[h][3] = fma(A, (double)x[u][h].w, acc[h][3]);
                 }
+        }
+        // dK: the lane owning the entry, f64, fixed entry -> lane map
+        if (has) {
+#pragma unroll
+            for (int d = 0; d < DK; ++d) dk[d] += (double)aw.y * ((double)qi[d] - (double)kj[d]);
         }
     }
 #pragma unroll
     for (int o = P; o < 32; o <<= 1)
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int h = 0; h < CH; ++h)
 #pragma unroll
             for (int c = 0; c < 4; ++c) acc[h][c] += __shfl_xor_sync(FULL, acc[h][c], o);
     if (grp == 0) {
         float* dvrow = a.dV + gk * (int64_t)dv;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < CH; ++h) {
             const int ch = l + h * P;
             if (ch < nch)
                 reinterpret_cast<float4*>(dvrow)[ch] =
@@ -396,12 +419,26 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     a.ws = ws;
     const int P = lanes_per_row(p->d_v);
     const unsigned qgrid = (unsigned)((total + BWD_WARPS - 1) / BWD_WARPS);
-#define ONEDF_BWDQ(PV) ONEDF_DISPATCH_DK(p->d_k, { bwd_query_kernel<DK, PV><<<qgrid, BWD_THREADS, 0, st>>>(a); })
+#define ONEDF_BWDQR(PV, RV)                                                                            \
+    ONEDF_DISPATCH_DK(p->d_k, {                                                                        \
+        if constexpr (PV == 32) {                                                                      \
+            if (p->d_v > 128) bwd_query_kernel<DK, PV, 2, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);        \
+            else bwd_query_kernel<DK, PV, 1, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);                    \
+        } else {                                                                                       \
+            bwd_query_kernel<DK, PV, 1, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);                         \
+        }                                                                                              \
+    })
+#define ONEDF_BWDQ(PV)                      \
+    if (p->k <= 32) { ONEDF_BWDQR(PV, 1) }  \
+    else if (p->k <= 64) { ONEDF_BWDQR(PV, 2) } \
+    else if (p->k <= 128) { ONEDF_BWDQR(PV, 4) } \
+    else { ONEDF_BWDQR(PV, 8) }
     if (P == 4) { ONEDF_BWDQ(4) }
     else if (P == 8) { ONEDF_BWDQ(8) }
     else if (P == 16) { ONEDF_BWDQ(16) }
     else { ONEDF_BWDQ(32) }
 #undef ONEDF_BWDQ
+#undef ONEDF_BWDQR
     tr.mark(1, st);
     e = launch_transpose(p, idx, t, st);
     if (e != cudaSuccess) return e;
@@ -410,7 +447,15 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     ka.Q = Q; ka.K = K; ka.dO = dO; ka.coeff = b->coeff; ka.slots = t->slots; ka.offsets = t->offsets;
     ka.korder = perm;
     ka.dK = dK; ka.dV = dV; ka.N = N; ka.L = N * (int64_t)p->k; ka.total = total; ka.k = p->k; ka.dv = p->d_v;
-#define ONEDF_BWDK(PV) ONEDF_DISPATCH_DK(p->d_k, { bwd_key_kernel<DK, PV><<<qgrid, BWD_THREADS, 0, st>>>(ka); })
+#define ONEDF_BWDK(PV)                                                                                 \
+    ONEDF_DISPATCH_DK(p->d_k, {                                                                        \
+        if constexpr (PV == 32) {                                                                      \
+            if (p->d_v > 128) bwd_key_kernel<DK, PV, 2><<<qgrid, BWD_THREADS, 0, st>>>(ka);            \
+            else bwd_key_kernel<DK, PV, 1><<<qgrid, BWD_THREADS, 0, st>>>(ka);                         \
+        } else {                                                                                       \
+            bwd_key_kernel<DK, PV, 1><<<qgrid, BWD_THREADS, 0, st>>>(ka);                              \
+        }                                                                                              \
+    })
     if (P == 4) { ONEDF_BWDK(4) }
     else if (P == 8) { ONEDF_BWDK(8) }
     else if (P == 16) { ONEDF_BWDK(16) }

@@ -307,9 +307,9 @@ __global__ void __launch_bounds__(1024) tr_scan_kernel(const TrArgs a) {
     for (int64_t t = t0; t < t1; ++t) { const uint32_t x = h[t]; h[t] = run; run += x; }
 }
 
-__global__ void __launch_bounds__(TR_THREADS) tr_downsweep_kernel(const TrArgs a) {
+__global__ void __launch_bounds__(TR_THREADS, 4) tr_downsweep_kernel(const TrArgs a) {
     __shared__ uint32_t sk[TR_TILE], sv[TR_TILE];
-    __shared__ uint32_t cnt[TR_RADIX * TR_WARPS];    // [digit][warp]
+    __shared__ uint32_t cnt[TR_WARPS * TR_RADIX];    // [warp][digit]: a warp's random digits hit distinct banks
     __shared__ uint32_t tstart[TR_RADIX], gbase[TR_RADIX];
     __shared__ uint32_t s_w[TR_WARPS];
     const int64_t bh = blockIdx.y, tile = blockIdx.x;
@@ -336,10 +336,10 @@ __global__ void __launch_bounds__(TR_THREADS) tr_downsweep_kernel(const TrArgs a
         const uint32_t d = act[r] ? ((key[r] >> a.shift) & 0xffu) : (uint32_t)TR_RADIX + lane;
         const unsigned peers = __match_any_sync(FULL, d);
         uint32_t prev = 0;
-        if (act[r]) prev = cnt[d * TR_WARPS + w];
+        if (act[r]) prev = cnt[w * TR_RADIX + d];
         rank[r] = prev + __popc(peers & lanemask_lt());
         __syncwarp();
-        if (act[r] && lane == __ffs(peers) - 1) cnt[d * TR_WARPS + w] = prev + __popc(peers);
+        if (act[r] && lane == __ffs(peers) - 1) cnt[w * TR_RADIX + d] = prev + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
@@ -348,12 +348,12 @@ __global__ void __launch_bounds__(TR_THREADS) tr_downsweep_kernel(const TrArgs a
         const int d = threadIdx.x;
         uint32_t pw[TR_WARPS], td = 0;
 #pragma unroll
-        for (int x = 0; x < TR_WARPS; ++x) { pw[x] = td; td += cnt[d * TR_WARPS + x]; }
+        for (int x = 0; x < TR_WARPS; ++x) { pw[x] = td; td += cnt[x * TR_RADIX + d]; }
         uint32_t ex;
         tr_block_scan(td, ex, s_w);
         tstart[d] = ex;
 #pragma unroll
-        for (int x = 0; x < TR_WARPS; ++x) cnt[d * TR_WARPS + x] = ex + pw[x];
+        for (int x = 0; x < TR_WARPS; ++x) cnt[x * TR_RADIX + d] = ex + pw[x];
     }
     __syncthreads();
     int ntile = 0;
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(TR_THREADS) tr_downsweep_kernel(const TrArgs a
     for (int r = 0; r < TR_IPT; ++r) {
         if (act[r]) {
             const uint32_t d = (key[r] >> a.shift) & 0xffu;
-            const uint32_t lp = cnt[d * TR_WARPS + w] + rank[r];
+            const uint32_t lp = cnt[w * TR_RADIX + d] + rank[r];
             sk[lp] = key[r];
             sv[lp] = val[r];
         }

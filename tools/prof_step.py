@@ -40,7 +40,7 @@ def main():
         sc, pm = onedf.sort(p, kc, ws=ws)
         O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws)
         if not a.fwd_only:
-            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws)
+            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qcode=qc, perm=pm)
     torch.cuda.synchronize()
     print("done", a.config)
 

@@ -34,7 +34,7 @@ for _ in range(a.reps + 1):
     O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws)
     e1.record()
     if a.bwd:
-        onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws)
+        onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qcode=qc, perm=pm)
     e2.record()
     torch.cuda.synchronize()
     ts.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
