@@ -45,10 +45,11 @@ constexpr int FWD_THREADS = FWD_WARPS * 32;
 #define ONEDF_FWD_UB 4
 #endif
 #ifndef ONEDF_FWD_MINB
-#define ONEDF_FWD_MINB 3
+#define ONEDF_FWD_MINB 4
 #endif
 constexpr int FWD_QPW = ONEDF_FWD_QPW;              // queries per warp (schedule stretch per CTA = 8*QPW)
 constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 loaded ahead (W = 128 -> one window)
+constexpr int FWD_CAP = 256;                        // pass-2 collection capacity per warp
 constexpr unsigned long long KEY_MAX = ~0ull;
 
 void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f) {
@@ -149,17 +150,120 @@ struct FwdArgs {
     void* ws;
 };
 
+// Per-query view of the candidate set C_i (A5): the admissible runs, their
+// windows, and a visitor that streams every candidate of C_i through a
+// callback in fixed (run, rank) order, FWD_UB batches of 32 at a time.
+template <int DK>
+struct CandSet {
+    const float* q;
+    uint64_t qc;
+    const uint64_t* scode;       // this (b,h) row
+    const float4* recs4;         // this (b,h) row of sorted key records
+    int64_t N, M, nruns;
+    int W, causal;
+
+    // lane c of the warp: window (base, w) of run c0 + c (lower_bound, D2/D3)
+    __device__ __forceinline__ void window(int64_t c, int64_t& base, int& w) const {
+        base = 0;
+        w = 0;
+        if (c < nruns) {
+            const int64_t s0 = causal ? c * M : 0;
+            const int64_t len = causal ? min64(M, N - s0) : N;
+            int64_t lo = 0, hi = len;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (__ldg(scode + s0 + mid) < qc) lo = mid + 1; else hi = mid;
+            }
+            const int64_t ww = min64(W, len);
+            int64_t st = lo - W / 2;
+            st = st < 0 ? 0 : st;
+            st = st > len - ww ? len - ww : st;
+            base = s0 + st;
+            w = (int)ww;
+        }
+    }
+
+    // One stretch of FWD_UB batches of 32 window entries starting at rank r0.
+    template <bool FULL, class F>
+    __device__ __forceinline__ bool stretch(const float4* wp, int r0, int ww, F&& f) const {
+        constexpr int REC = RecW<DK>::value;
+        const int lane = lane_id();
+        float D[FWD_UB];
+        int jj[FWD_UB];
+        bool ok[FWD_UB];
+#pragma unroll
+        for (int u = 0; u < FWD_UB; ++u) {
+            ok[u] = FULL || r0 + 32 * u + lane < ww;
+            D[u] = 0.f;
+            jj[u] = 0;
+            if (ok[u]) {
+                float rv[REC];
+#pragma unroll
+                for (int v = 0; v < REC / 4; ++v) {
+                    const float4 t4 = __ldg(wp + (r0 + 32 * u) * (REC / 4) + v);
+                    rv[4 * v] = t4.x; rv[4 * v + 1] = t4.y; rv[4 * v + 2] = t4.z; rv[4 * v + 3] = t4.w;
+                }
+                D[u] = rank_dist32<DK>(q, rv);
+                jj[u] = __float_as_int(rv[DK]);
+            }
+        }
+        return f(D, jj, ok, r0, ww);
+    }
+
+    // f(D[FWD_UB], j[FWD_UB], valid[FWD_UB]) per stretch; returns false to stop.
+    // (base0, w0) are the lane-parallel windows of runs 0..31, computed once.
+    template <class F>
+    __device__ __forceinline__ bool visit(int64_t base0, int w0, F&& f) const {
+        constexpr int REC = RecW<DK>::value;
+        const int lane = lane_id();
+        for (int64_t c0 = 0; c0 < nruns; c0 += 32) {
+            int64_t base = base0;
+            int w = w0;
+            if (c0 > 0) window(c0 + lane, base, w);
+            const int nc = (int)min64(32, nruns - c0);
+            for (int cc = 0; cc < nc; ++cc) {
+                const int b = (int)__shfl_sync(FULL, base, cc);
+                const int ww = __shfl_sync(FULL, w, cc);
+                const float4* wp = recs4 + (b + lane) * (REC / 4);
+                if (ww % (32 * FWD_UB) == 0) {
+                    // full stretches (the common case: W = 128 = 4 x 32): no per-lane bounds checks
+                    for (int r0 = 0; r0 < ww; r0 += 32 * FWD_UB) {
+                        if (!stretch<true>(wp, r0, ww, f)) return false;
+                    }
+                } else {
+                    for (int r0 = 0; r0 < ww; r0 += 32 * FWD_UB) {
+                        if (!stretch<false>(wp, r0, ww, f)) return false;
+                    }
+                }
+            }
+        }
+        return true;
+    }
+};
+
+__device__ __forceinline__ unsigned long long make_key(float D, int j) {
+    return ((unsigned long long)__float_as_uint(D) << 32) | (unsigned)j;
+}
+
+// Pass 1 list length per lane: the union of the per-lane lists (32 L values)
+// must hold at least k of them; L = 2 * ceil(k/32) gives 2k.
+template <int R>
+struct PassOne { static constexpr int L = 2 * R; };
+
 template <int DK, int R>
 __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_kernel(const FwdArgs a) {
-    constexpr int REC = RecW<DK>::value;
-    __shared__ __align__(16) unsigned long long s_pend[FWD_WARPS][32];
+    constexpr int L = PassOne<R>::L;
+    __shared__ __align__(16) unsigned long long s_buf[FWD_WARPS][FWD_CAP + 32 * FWD_UB];
+    __shared__ __align__(16) unsigned long long s_top[FWD_WARPS][32 * R];
     const int warp = threadIdx.x / 32, lane = lane_id();
-    unsigned long long* pend = s_pend[warp];
+    unsigned long long* buf = s_buf[warp];
+    unsigned long long* stop = s_top[warp];
     const float e = __ldg(a.eps);
     if (blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
     const double ed = (double)e;
     const int64_t N = a.N;
     const int k = a.k;
+    constexpr int REC = RecW<DK>::value;
 
     for (int u = 0; u < FWD_QPW; ++u) {
         const int64_t slot = ((int64_t)blockIdx.x * FWD_QPW + u) * FWD_WARPS + warp;
@@ -171,91 +275,146 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         float q[DK];
 #pragma unroll
         for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
-        const uint64_t qc = __ldg(a.qcode + gq);
+        CandSet<DK> cs;
+        cs.q = q;
+        cs.qc = __ldg(a.qcode + gq);
+        cs.scode = a.scode + bh * N;
+        cs.recs4 = reinterpret_cast<const float4*>(a.recs + bh * N * REC);
+        cs.N = N; cs.M = a.M; cs.W = a.W; cs.causal = a.causal;
+        cs.nruns = a.causal ? i / a.M : 1;
+        int64_t base0;
+        int w0;
+        cs.window(lane, base0, w0);
+
+        // ---------------- A6 pass 1: per-lane L smallest D (f32 min/max chain).
+        // The k-th smallest of the union of these lists is an upper bound T on
+        // the k-th smallest D of C_i (k distinct candidates lie at or below it).
+        float lst[L];
+#pragma unroll
+        for (int t = 0; t < L; ++t) lst[t] = INFINITY;
+        cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&)[FWD_UB], const bool (&ok)[FWD_UB], int, int) {
+#pragma unroll
+            for (int uu = 0; uu < FWD_UB; ++uu) {
+                float x = ok[uu] ? D[uu] : INFINITY;
+#pragma unroll
+                for (int t = 0; t < L; ++t) {
+                    const float lo = fminf(lst[t], x);
+                    x = fmaxf(lst[t], x);
+                    lst[t] = lo;
+                }
+            }
+            return true;
+        });
+        // T: a bit pattern with #{values <= T} >= k (non-negative floats order as
+        // their bits).  Bisection between the smallest list head and the largest
+        // list tail, stopped at ~2^-8 relative resolution: any such T is a valid
+        // bound, a slightly larger one only admits a few more keys in pass 2.
+        unsigned tb;
+        {
+            float fmn = lst[0], fmx = lst[L - 1];
+            unsigned finite = 0;
+#pragma unroll
+            for (int t = 0; t < L; ++t) finite += lst[t] < INFINITY;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) fmn = fminf(fmn, __shfl_xor_sync(FULL, fmn, o));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
+            if (__reduce_add_sync(FULL, finite) < (unsigned)k) {
+                tb = 0x7f800000u;                          // fewer than k candidates: admit all
+            } else {
+                unsigned lo = __float_as_uint(fmn), hi = __float_as_uint(fmx);   // count(<= hi) >= k
+#pragma unroll 1
+                while (hi - lo > (1u << 15)) {          // 2^-8 of a mantissa step
+                    const unsigned mid = lo + ((hi - lo) >> 1);
+                    unsigned c = 0;
+#pragma unroll
+                    for (int t = 0; t < L; ++t) c += __float_as_uint(lst[t]) <= mid;
+                    if (__reduce_add_sync(FULL, c) >= (unsigned)k) hi = mid; else lo = mid + 1;
+                }
+                tb = hi;
+            }
+        }
+
+        // ---------------- A6 pass 2: collect every candidate with D <= T (order is
+        // irrelevant: the final order comes from ranking the unique keys)
+        int cnt = 0;
+        const bool fits = cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB],
+                                                  const bool (&ok)[FWD_UB], int, int) {
+#pragma unroll
+            for (int uu = 0; uu < FWD_UB; ++uu) {
+                const bool pass = ok[uu] && __float_as_uint(D[uu]) <= tb;
+                const unsigned m = __ballot_sync(FULL, pass);
+                if (pass) buf[cnt + __popc(m & lanemask_lt())] = make_key(D[uu], jj[uu]);
+                cnt += __popc(m);
+            }
+            return cnt <= FWD_CAP;                     // buf has FWD_CAP + 32*FWD_UB slots
+        });
+        __syncwarp();
+        if (fits) {
+            // ---------------- exact order of the collected keys by counting (keys are unique)
+            for (int t = lane; t < 32 * R; t += 32) stop[t] = KEY_MAX;
+            __syncwarp();
+            // each lane ranks its elements e = m*32 + lane against all cnt keys
+            const int mm = (cnt + 31) / 32;
+            for (int m = 0; m < mm; ++m) {
+                const int e2 = m * 32 + lane;
+                const unsigned long long mine = e2 < cnt ? buf[e2] : KEY_MAX;
+                int rank = 0;
+                const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(buf);
+                int x = 0;
+                for (; x + 4 <= cnt; x += 4) {
+                    const ulonglong2 y0 = b2[x / 2], y1 = b2[x / 2 + 1];
+                    rank += (y0.x < mine) + (y0.y < mine) + (y1.x < mine) + (y1.y < mine);
+                }
+                for (; x < cnt; ++x) rank += buf[x] < mine;
+                if (e2 < cnt && rank < k) stop[rank] = mine;
+            }
+        } else {
+            // ---------------- rare: too many keys at or below T (e.g. many equal
+            // distances) -- streaming selection with shuffle-bitonic merges,
+            // starting from the same bound
+            unsigned long long top[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) top[r] = KEY_MAX;
+            unsigned long long thresh = tb >= 0x7f800000u ? KEY_MAX : ((unsigned long long)(tb + 1u) << 32);
+            unsigned long long* pend = buf;
+            int pc = 0;
+            cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB], const bool (&ok)[FWD_UB], int,
+                                    int) {
+#pragma unroll
+                for (int uu = 0; uu < FWD_UB; ++uu) {
+                    const unsigned long long key = ok[uu] ? make_key(D[uu], jj[uu]) : KEY_MAX;
+                    bool pass = key < thresh;
+                    unsigned m = __ballot_sync(FULL, pass);
+                    if (m == 0) continue;
+                    int n = __popc(m);
+                    if (pc + n > 32) {
+                        __syncwarp();
+                        merge_pending<R>(top, lane < pc ? pend[lane] : KEY_MAX);
+                        thresh = umin64(thresh, list_get<R>(top, k - 1));
+                        pc = 0;
+                        pass = key < thresh;
+                        m = __ballot_sync(FULL, pass);
+                        n = __popc(m);
+                    }
+                    if (pass) pend[pc + __popc(m & lanemask_lt())] = key;
+                    pc += n;
+                    __syncwarp();
+                }
+                return true;
+            });
+            if (pc > 0) {
+                __syncwarp();
+                merge_pending<R>(top, lane < pc ? pend[lane] : KEY_MAX);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) stop[r * 32 + lane] = top[r];
+        }
+        __syncwarp();
         unsigned long long top[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) top[r] = KEY_MAX;
-
-        // ---------------- A5 + A6: candidate search and exact top-k
-        const int64_t nruns = a.causal ? i / a.M : 1;
-        const uint64_t* scode = a.scode + bh * N;
-        const float4* recs4 = reinterpret_cast<const float4*>(a.recs + bh * N * REC);
-        unsigned long long thresh = KEY_MAX;
-        int cnt = 0;
-        for (int64_t c0 = 0; c0 < nruns; c0 += 32) {
-            const int64_t c = c0 + lane;
-            int64_t base = 0;
-            int w = 0;
-            if (c < nruns) {
-                const int64_t s0 = a.causal ? c * a.M : 0;
-                const int64_t len = a.causal ? min64(a.M, N - s0) : N;
-                int64_t lo = 0, hi = len;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (__ldg(scode + s0 + mid) < qc) lo = mid + 1; else hi = mid;
-                }
-                const int64_t ww = min64(a.W, len);
-                int64_t s = lo - a.W / 2;
-                s = s < 0 ? 0 : s;
-                s = s > len - ww ? len - ww : s;
-                base = s0 + s;
-                w = (int)ww;
-            }
-            const int nc = (int)min64(32, nruns - c0);
-            for (int cc = 0; cc < nc; ++cc) {
-                const int b = (int)__shfl_sync(FULL, base, cc);   // offset inside this (b,h) row
-                const int ww = __shfl_sync(FULL, w, cc);
-                const float4* wp = recs4 + (size_t)(b + lane) * (REC / 4);
-                for (int r0 = 0; r0 < ww; r0 += 32 * FWD_UB) {
-                    // all loads of up to FWD_UB batches first (memory-level parallelism),
-                    // then ONE vote for the whole stretch: most stretches hold no key below
-                    // the running k-th once the list has warmed up
-                    unsigned long long key[FWD_UB];
-#pragma unroll
-                    for (int u = 0; u < FWD_UB; ++u) {
-                        const int r = r0 + 32 * u + lane;
-                        key[u] = KEY_MAX;
-                        if (r < ww) {
-                            float rv[REC];
-#pragma unroll
-                            for (int v = 0; v < REC / 4; ++v) {
-                                const float4 t4 = __ldg(wp + (size_t)(r0 + 32 * u) * (REC / 4) + v);
-                                rv[4 * v] = t4.x; rv[4 * v + 1] = t4.y; rv[4 * v + 2] = t4.z; rv[4 * v + 3] = t4.w;
-                            }
-                            const float D = rank_dist32<DK>(q, rv);
-                            key[u] = ((unsigned long long)__float_as_uint(D) << 32) | (unsigned)__float_as_int(rv[DK]);
-                        }
-                    }
-                    unsigned long long kmin = key[0];
-#pragma unroll
-                    for (int u = 1; u < FWD_UB; ++u) kmin = umin64(kmin, key[u]);
-                    if (!__any_sync(FULL, kmin < thresh)) continue;
-#pragma unroll
-                    for (int u = 0; u < FWD_UB; ++u) {
-                        bool pass = key[u] < thresh;
-                        unsigned m = __ballot_sync(FULL, pass);
-                        if (m == 0) continue;
-                        int n = __popc(m);
-                        if (cnt + n > 32) {
-                            __syncwarp();
-                            merge_pending<R>(top, lane < cnt ? pend[lane] : KEY_MAX);
-                            thresh = list_get<R>(top, k - 1);
-                            cnt = 0;
-                            pass = key[u] < thresh;
-                            m = __ballot_sync(FULL, pass);
-                            n = __popc(m);
-                        }
-                        if (pass) pend[cnt + __popc(m & lanemask_lt())] = key[u];
-                        cnt += n;
-                    }
-                }
-            }
-        }
-        if (cnt > 0) {
-            __syncwarp();
-            merge_pending<R>(top, lane < cnt ? pend[lane] : KEY_MAX);
-        }
-        __syncwarp();   // pend is rewritten by the next query
+        for (int r = 0; r < R; ++r) top[r] = stop[r * 32 + lane];
+        __syncwarp();   // buf/stop are rewritten by the next query
 
         // ---------------- outputs: idx row (slot e = r*32 + lane), valid count
         int32_t* idx_row = a.idx + gq * k;

@@ -8,182 +8,209 @@
 // with dKbar_i = w_mu,i (q_i - Kbar_i) and dVbar_i = A_mu,i dO_i emitted by
 // the backward query pass (non-causal: (1/N) sum over all i).
 //
-// Both are 3-phase blocked scans with a FIXED combination order (block sums
-// -> sequential scan over blocks -> in-block sequential scan), so results are
-// deterministic.  Threads map to columns, rows run sequentially, so every
-// warp access to a d_v-wide row is one coalesced 128-B line.
+// One column-scan engine serves both, per matrix [B*H][N][C] (C = d_k or
+// d_v): tiles of SCAN_TB rows x C columns; a 256-thread CTA maps thread
+// (g, c) to column c of row-group g (CW = pow2 >= C columns, RG = 256/CW
+// row-groups of SCAN_TB/RG consecutive rows), so each warp access to a row
+// is one coalesced line.  Three launches with a FIXED combination order:
+// (1) tile sums (rows of a row-group sequential, row-groups in order),
+// (2) exclusive scan over tiles per column, (3) apply: each thread re-walks
+// its rows from (tile prefix + earlier row-groups) and writes the running
+// value.  Deterministic; the tile is L1-resident for the second walk.
 #include "common.cuh"
 #include "internal.h"
 
 namespace onedf {
 
-constexpr int MEAN_TB = 128;   // rows per scan block
+constexpr int SCAN_TB = 256;        // rows per tile
+constexpr int SCAN_THREADS = 256;
 
-static int64_t mean_blocks(const onedf_problem* p) { return (p->N + MEAN_TB - 1) / MEAN_TB; }
+static int64_t scan_tiles(const onedf_problem* p) { return (p->N + SCAN_TB - 1) / SCAN_TB; }
 
 void mean_carve(const onedf_problem* p, Carver* c, MeanBufs* m) {
     const int64_t BH = p->B * p->H;
     const int64_t rows = p->causal ? p->N : 1;
     m->Kbar = c->take<float>((size_t)(BH * rows * p->d_k));
     m->Vbar = c->take<float>((size_t)(BH * rows * p->d_v));
-    m->part = c->take<double>((size_t)(BH * (mean_blocks(p) + 1) * (p->d_k + p->d_v)));
+    m->part = c->take<double>((size_t)(BH * (scan_tiles(p) + 1) * (p->d_k + p->d_v)));
 }
 
-// ------------------------------------------------------------------ forward prefix means
-__global__ void mean_block_sums_kernel(const float* __restrict__ K, const float* __restrict__ V, int64_t N, int dk,
-                                       int dv, int64_t nblk, double* __restrict__ part) {
-    const int64_t bh = blockIdx.y, blk = blockIdx.x;
-    const int W = dk + dv;
-    const int64_t r0 = blk * MEAN_TB, r1 = min64(N, r0 + MEAN_TB);
-    for (int c = threadIdx.x; c < W; c += blockDim.x) {
-        double acc = 0.0;
-        if (c < dk) {
-            for (int64_t r = r0; r < r1; ++r) acc += (double)K[(bh * N + r) * dk + c];
-        } else {
-            const int cv = c - dk;
-            for (int64_t r = r0; r < r1; ++r) acc += (double)V[(bh * N + r) * dv + cv];
-        }
-        part[(bh * (nblk + 1) + blk) * W + c] = acc;
+static int pow2_at_least(int c) {
+    int w = 1;
+    while (w < c) w <<= 1;
+    return w;
+}
+
+// Value of row i, column c of the scanned matrix.
+//   MODE 0 (A4):  X[i][c]                                 (K or V itself)
+//   MODE 1 (A11, K columns): w_mu,i (q_i[c] - Kbar_i[c]) * s_i
+//   MODE 2 (A11, V columns): A_mu,i dO_i[c] * s_i        s_i = 1/(i+1) causal, 1 otherwise
+struct ScanSrc {
+    const float* X;       // MODE 0: K or V; MODE 1: Q; MODE 2: dO
+    const float* Kbar;    // MODE 1
+    const float2* muco;   // MODE 1, 2
+    int C, causal;
+};
+
+template <int MODE>
+__device__ __forceinline__ double scan_value(const ScanSrc& s, int64_t bh, int64_t N, int64_t i, int c) {
+    const int64_t row = bh * N + i;
+    if (MODE == 0) return (double)__ldg(s.X + row * s.C + c);
+    const float2 mc = __ldg(s.muco + row);
+    double y;
+    if (MODE == 1) {
+        const float kb = __ldg(s.Kbar + (bh * (s.causal ? N : 1) + (s.causal ? i : 0)) * s.C + c);
+        y = (double)mc.y * ((double)__ldg(s.X + row * s.C + c) - (double)kb);
+    } else {
+        y = (double)mc.x * (double)__ldg(s.X + row * s.C + c);
+    }
+    return s.causal ? y / (double)(i + 1) : y;
+}
+
+// (1) tile sums -> part[bh][tile][c]
+template <int MODE>
+__global__ void __launch_bounds__(SCAN_THREADS) scan_tile_sums_kernel(const ScanSrc s, int64_t N, int64_t ntile,
+                                                                      int CW, double* __restrict__ part) {
+    __shared__ double sh[SCAN_THREADS];
+    const int64_t bh = blockIdx.y, tile = blockIdx.x;
+    const int c = threadIdx.x % CW, g = threadIdx.x / CW, RG = SCAN_THREADS / CW;
+    const int per = SCAN_TB / RG;
+    const int64_t r0 = tile * SCAN_TB + (int64_t)g * per, r1 = min64(N, r0 + per);
+    double acc = 0.0;
+    if (c < s.C)
+        for (int64_t r = r0; r < r1; ++r) acc += scan_value<MODE>(s, bh, N, r, c);
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    if (g == 0 && c < s.C) {
+        double t = 0.0;
+        for (int x = 0; x < RG; ++x) t += sh[x * CW + c];
+        part[(bh * (ntile + 1) + tile) * s.C + c] = t;
     }
 }
 
-// exclusive scan over blocks (forward direction); part[nblk] = total
-__global__ void mean_scan_blocks_kernel(double* __restrict__ part, int64_t nblk, int W, int64_t N, int causal,
-                                        float* __restrict__ Kbar, float* __restrict__ Vbar, int dk, int dv) {
+// (2) per (bh, column): exclusive scan over tiles (forward) or suffix scan
+// (reverse); part[ntile] = total.
+__global__ void scan_tiles_kernel(double* __restrict__ part, int64_t ntile, int C, int reverse) {
     const int64_t bh = blockIdx.x;
-    for (int c = threadIdx.x; c < W; c += blockDim.x) {
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
         double run = 0.0;
-        for (int64_t b = 0; b < nblk; ++b) {
-            double* x = part + (bh * (nblk + 1) + b) * W + c;
-            double t = *x;
+        for (int64_t u = 0; u < ntile; ++u) {
+            const int64_t b = reverse ? ntile - 1 - u : u;
+            double* x = part + (bh * (ntile + 1) + b) * C + c;
+            const double t = *x;
             *x = run;
             run += t;
         }
-        part[(bh * (nblk + 1) + nblk) * W + c] = run;
-        if (!causal) {
-            const float mean = (float)(run / (double)N);
-            if (c < dk) Kbar[bh * dk + c] = mean;
-            else Vbar[bh * dv + (c - dk)] = mean;
-        }
+        part[(bh * (ntile + 1) + ntile) * C + c] = run;
     }
 }
 
-__global__ void mean_write_kernel(const float* __restrict__ K, const float* __restrict__ V, int64_t N, int dk, int dv,
-                                  int64_t nblk, const double* __restrict__ part, float* __restrict__ Kbar,
-                                  float* __restrict__ Vbar) {
-    const int64_t bh = blockIdx.y, blk = blockIdx.x;
-    const int W = dk + dv;
-    const int64_t r0 = blk * MEAN_TB, r1 = min64(N, r0 + MEAN_TB);
-    for (int c = threadIdx.x; c < W; c += blockDim.x) {
-        double acc = part[(bh * (nblk + 1) + blk) * W + c];
-        if (c < dk) {
-            for (int64_t r = r0; r < r1; ++r) {
-                acc += (double)K[(bh * N + r) * dk + c];
-                Kbar[(bh * N + r) * dk + c] = (float)(acc / (double)(r + 1));
-            }
-        } else {
-            const int cv = c - dk;
-            for (int64_t r = r0; r < r1; ++r) {
-                acc += (double)V[(bh * N + r) * dv + cv];
-                Vbar[(bh * N + r) * dv + cv] = (float)(acc / (double)(r + 1));
-            }
-        }
+// (3a) A4 apply: out[i] = (prefix through i) / (i + 1)  (causal only)
+__global__ void __launch_bounds__(SCAN_THREADS) mean_apply_kernel(const ScanSrc s, int64_t N, int64_t ntile, int CW,
+                                                                  const double* __restrict__ part,
+                                                                  float* __restrict__ out) {
+    __shared__ double sh[SCAN_THREADS];
+    const int64_t bh = blockIdx.y, tile = blockIdx.x;
+    const int c = threadIdx.x % CW, g = threadIdx.x / CW, RG = SCAN_THREADS / CW;
+    const int per = SCAN_TB / RG;
+    const int64_t r0 = tile * SCAN_TB + (int64_t)g * per, r1 = min64(N, r0 + per);
+    const bool on = c < s.C;
+    double own = 0.0;
+    if (on)
+        for (int64_t r = r0; r < r1; ++r) own += scan_value<0>(s, bh, N, r, c);
+    sh[threadIdx.x] = own;
+    __syncthreads();
+    if (!on) return;
+    double run = part[(bh * (ntile + 1) + tile) * s.C + c];
+    for (int x = 0; x < g; ++x) run += sh[x * CW + c];
+    for (int64_t r = r0; r < r1; ++r) {
+        run += scan_value<0>(s, bh, N, r, c);
+        out[(bh * N + r) * s.C + c] = (float)(run / (double)(r + 1));
     }
 }
 
-static int mean_threads(int W) { return W <= 64 ? 64 : (W <= 128 ? 128 : 256); }
+__global__ void mean_global_kernel(const double* __restrict__ part, int64_t ntile, int C, int64_t N,
+                                   float* __restrict__ out) {
+    const int64_t bh = blockIdx.x;
+    for (int c = threadIdx.x; c < C; c += blockDim.x)
+        out[bh * C + c] = (float)(part[(bh * (ntile + 1) + ntile) * C + c] / (double)N);
+}
+
+// (3b) A11 apply: D[t] += sum_{i >= t} y_i (causal, reverse walk) or
+// D[t] += (1/N) sum_i y_i (non-causal).
+template <int MODE>
+__global__ void __launch_bounds__(SCAN_THREADS) grad_apply_kernel(const ScanSrc s, int64_t N, int64_t ntile, int CW,
+                                                                  const double* __restrict__ part,
+                                                                  float* __restrict__ D) {
+    __shared__ double sh[SCAN_THREADS];
+    const int64_t bh = blockIdx.y, tile = blockIdx.x;
+    const int c = threadIdx.x % CW, g = threadIdx.x / CW, RG = SCAN_THREADS / CW;
+    const int per = SCAN_TB / RG;
+    const int64_t r0 = tile * SCAN_TB + (int64_t)g * per, r1 = min64(N, r0 + per);
+    const bool on = c < s.C;
+    if (!s.causal) {
+        if (!on) return;
+        const double add = part[(bh * (ntile + 1) + ntile) * s.C + c] / (double)N;
+        for (int64_t r = r0; r < r1; ++r) {
+            float* o = D + (bh * N + r) * s.C + c;
+            *o = (float)((double)*o + add);
+        }
+        return;
+    }
+    double own = 0.0;
+    if (on)
+        for (int64_t r = r0; r < r1; ++r) own += scan_value<MODE>(s, bh, N, r, c);
+    sh[threadIdx.x] = own;
+    __syncthreads();
+    if (!on) return;
+    double run = part[(bh * (ntile + 1) + tile) * s.C + c];    // sum over later tiles
+    for (int x = RG - 1; x > g; --x) run += sh[x * CW + c];      // later row-groups of this tile
+    for (int64_t r = r1 - 1; r >= r0; --r) {
+        run += scan_value<MODE>(s, bh, N, r, c);
+        float* o = D + (bh * N + r) * s.C + c;
+        *o = (float)((double)*o + run);
+    }
+}
 
 cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const float* V, MeanBufs* m,
                                 cudaStream_t st) {
-    const int64_t BH = p->B * p->H, N = p->N, nblk = mean_blocks(p);
-    const int dk = p->d_k, dv = p->d_v, W = dk + dv;
-    const int th = mean_threads(W);
-    mean_block_sums_kernel<<<dim3((unsigned)nblk, (unsigned)BH), th, 0, st>>>(K, V, N, dk, dv, nblk, m->part);
-    mean_scan_blocks_kernel<<<(unsigned)BH, th, 0, st>>>(m->part, nblk, W, N, p->causal, m->Kbar, m->Vbar, dk, dv);
-    if (p->causal)
-        mean_write_kernel<<<dim3((unsigned)nblk, (unsigned)BH), th, 0, st>>>(K, V, N, dk, dv, nblk, m->part, m->Kbar,
-                                                                            m->Vbar);
-    return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ backward chain rule (A11)
-// y_i[c] = dKbar_i[c] (c < dk) or dVbar_i[c - dk]; scaled by 1/(i+1) when causal.
-__device__ __forceinline__ double mean_grad_y(int c, int64_t bh, int64_t i, int64_t N, int dk, int dv, int causal,
-                                              const float* __restrict__ Q, const float* __restrict__ Kbar,
-                                              const float* __restrict__ dO, const float2* __restrict__ muco) {
-    const float2 mc = muco[bh * N + i];
-    double y;
-    if (c < dk) {
-        const float kb = Kbar[(bh * (causal ? N : 1) + (causal ? i : 0)) * dk + c];
-        y = (double)mc.y * ((double)Q[(bh * N + i) * dk + c] - (double)kb);
+    const int64_t BH = p->B * p->H, N = p->N, nt = scan_tiles(p);
+    const dim3 grid((unsigned)nt, (unsigned)BH);
+    double* partK = m->part;
+    double* partV = m->part + BH * (nt + 1) * p->d_k;
+    const ScanSrc sk{K, nullptr, nullptr, p->d_k, p->causal};
+    const ScanSrc sv{V, nullptr, nullptr, p->d_v, p->causal};
+    const int cwk = pow2_at_least(p->d_k), cwv = pow2_at_least(p->d_v);
+    scan_tile_sums_kernel<0><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
+    scan_tile_sums_kernel<0><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV);
+    scan_tiles_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, 0);
+    scan_tiles_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, 0);
+    if (p->causal) {
+        mean_apply_kernel<<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, m->Kbar);
+        mean_apply_kernel<<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, m->Vbar);
     } else {
-        y = (double)mc.x * (double)dO[(bh * N + i) * dv + (c - dk)];
+        mean_global_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, N, m->Kbar);
+        mean_global_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, N, m->Vbar);
     }
-    return causal ? y / (double)(i + 1) : y;
-}
-
-__global__ void grad_block_sums_kernel(const float* __restrict__ Q, const float* __restrict__ Kbar,
-                                       const float* __restrict__ dO, const float2* __restrict__ muco, int64_t N,
-                                       int dk, int dv, int causal, int64_t nblk, double* __restrict__ part) {
-    const int64_t bh = blockIdx.y, blk = blockIdx.x;
-    const int W = dk + dv;
-    const int64_t r0 = blk * MEAN_TB, r1 = min64(N, r0 + MEAN_TB);
-    for (int c = threadIdx.x; c < W; c += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t r = r1 - 1; r >= r0; --r) acc += mean_grad_y(c, bh, r, N, dk, dv, causal, Q, Kbar, dO, muco);
-        part[(bh * (nblk + 1) + blk) * W + c] = acc;
-    }
-}
-
-// exclusive SUFFIX scan over blocks: part[b] = sum of blocks > b; part[nblk] = total
-__global__ void grad_scan_blocks_kernel(double* __restrict__ part, int64_t nblk, int W) {
-    const int64_t bh = blockIdx.x;
-    for (int c = threadIdx.x; c < W; c += blockDim.x) {
-        double run = 0.0;
-        for (int64_t b = nblk - 1; b >= 0; --b) {
-            double* x = part + (bh * (nblk + 1) + b) * W + c;
-            double t = *x;
-            *x = run;
-            run += t;
-        }
-        part[(bh * (nblk + 1) + nblk) * W + c] = run;
-    }
-}
-
-__global__ void grad_apply_kernel(const float* __restrict__ Q, const float* __restrict__ Kbar,
-                                  const float* __restrict__ dO, const float2* __restrict__ muco, int64_t N, int dk,
-                                  int dv, int causal, int64_t nblk, const double* __restrict__ part,
-                                  float* __restrict__ dK, float* __restrict__ dV) {
-    const int64_t bh = blockIdx.y, blk = blockIdx.x;
-    const int W = dk + dv;
-    const int64_t r0 = blk * MEAN_TB, r1 = min64(N, r0 + MEAN_TB);
-    for (int c = threadIdx.x; c < W; c += blockDim.x) {
-        float* out = c < dk ? dK + bh * N * dk + c : dV + bh * N * dv + (c - dk);
-        const int stride = c < dk ? dk : dv;
-        if (causal) {
-            double acc = part[(bh * (nblk + 1) + blk) * W + c];
-            for (int64_t r = r1 - 1; r >= r0; --r) {
-                acc += mean_grad_y(c, bh, r, N, dk, dv, causal, Q, Kbar, dO, muco);
-                out[r * stride] = (float)((double)out[r * stride] + acc);
-            }
-        } else {
-            const double add = part[(bh * (nblk + 1) + nblk) * W + c] / (double)N;
-            for (int64_t r = r0; r < r1; ++r) out[r * stride] = (float)((double)out[r * stride] + add);
-        }
-    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const float* dO, const float* muco,
                                   MeanBufs* m, float* dK, float* dV, cudaStream_t st) {
-    const int64_t BH = p->B * p->H, N = p->N, nblk = mean_blocks(p);
-    const int dk = p->d_k, dv = p->d_v, W = dk + dv;
-    const int th = mean_threads(W);
+    const int64_t BH = p->B * p->H, N = p->N, nt = scan_tiles(p);
+    const dim3 grid((unsigned)nt, (unsigned)BH);
     const float2* mc = reinterpret_cast<const float2*>(muco);
-    grad_block_sums_kernel<<<dim3((unsigned)nblk, (unsigned)BH), th, 0, st>>>(Q, m->Kbar, dO, mc, N, dk, dv,
-                                                                              p->causal, nblk, m->part);
-    grad_scan_blocks_kernel<<<(unsigned)BH, th, 0, st>>>(m->part, nblk, W);
-    grad_apply_kernel<<<dim3((unsigned)nblk, (unsigned)BH), th, 0, st>>>(Q, m->Kbar, dO, mc, N, dk, dv, p->causal,
-                                                                         nblk, m->part, dK, dV);
+    double* partK = m->part;
+    double* partV = m->part + BH * (nt + 1) * p->d_k;
+    const ScanSrc sk{Q, m->Kbar, mc, p->d_k, p->causal};
+    const ScanSrc sv{dO, nullptr, mc, p->d_v, p->causal};
+    const int cwk = pow2_at_least(p->d_k), cwv = pow2_at_least(p->d_v);
+    scan_tile_sums_kernel<1><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
+    scan_tile_sums_kernel<2><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV);
+    scan_tiles_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, 1);
+    scan_tiles_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, 1);
+    grad_apply_kernel<1><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, dK);
+    grad_apply_kernel<2><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, dV);
     return cudaGetLastError();
 }
 
