@@ -86,12 +86,12 @@ enum {
     ONEDF_OP_STEP_HOST = 4
 };
 
-/* Synchronous range checks of every field (no device work).  Also returns
- * ONEDF_ERR_UNSUPPORTED when a sorted run would exceed the largest segment
- * this build sorts (onedf_max_run_length()). */
+/* Synchronous range checks of every field (no device work). */
 onedf_status onedf_validate(const onedf_problem* p);
 
-/* Longest sorted run (M causal, N non-causal) the segmented sort handles. */
+/* Longest sorted run (M causal, N non-causal) the segmented sort keeps in
+ * shared memory; longer runs sort through global scratch in the workspace
+ * (onedf_workspace_size(p, ONEDF_OP_SORT) grows by 24 bytes per position). */
 int64_t onedf_max_run_length(void);
 
 /* Bytes of device workspace `op` needs (0 if the problem is invalid).  The

@@ -46,7 +46,6 @@ static onedf_status validate(const onedf_problem* p) {
     const int b = effective_bits(p);
     if (b < 1 || b > 32 || p->d_k * b > 63) return ONEDF_ERR_INVALID_ARG;
     if (p->N * (int64_t)p->k >= (1ll << 31)) return ONEDF_ERR_INVALID_ARG;
-    if (run_len_max(p) > SEG_SORT_MAX) return ONEDF_ERR_UNSUPPORTED;
     return ONEDF_OK;
 }
 
@@ -75,7 +74,12 @@ static size_t encode_bytes(const onedf_problem* p) {
     Carver c(nullptr);
     return encode_ws_bytes(p, &c);
 }
-static size_t sort_bytes(const onedf_problem*) { return WS_HEADER; }
+static size_t sort_bytes(const onedf_problem* p) {
+    Carver c(nullptr);
+    SortScratch s;
+    sort_carve(p, &c, &s);
+    return c.bytes();
+}
 
 struct StepLayout {
     float *Q, *K, *V, *dO, *O, *dQ, *dK, *dV, *Z, *eps;
@@ -129,8 +133,11 @@ static onedf_status do_encode(const onedf_problem* p, const float* Q, const floa
     return finish(launch_encode(p, effective_bits(p), Q, K, lohi_in, qcode, kcode, lohi_out, ws, &c, st));
 }
 static onedf_status do_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode, int32_t* perm,
-                            cudaStream_t st) {
-    return finish(launch_seg_sort(p, kcode, scode, perm, st));
+                            void* ws, cudaStream_t st) {
+    Carver c(ws);
+    SortScratch scr;
+    sort_carve(p, &c, &scr);
+    return finish(launch_seg_sort(p, kcode, scode, perm, scr, st));
 }
 static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                            const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
@@ -194,7 +201,7 @@ onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t*
     if (s != ONEDF_OK) return s;
     if (!kcode || !scode || !perm) return ONEDF_ERR_INVALID_ARG;
     if (cudaMemsetAsync(ws, 0, 4, (cudaStream_t)stream) != cudaSuccess) return finish(cudaGetLastError());
-    return do_sort(p, kcode, scode, perm, (cudaStream_t)stream);
+    return do_sort(p, kcode, scode, perm, ws, (cudaStream_t)stream);
 }
 
 onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V,
@@ -275,7 +282,7 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
     }
     if (e != cudaSuccess) return finish(e);
     if ((s = do_encode(p, L.Q, L.K, nullptr, L.qcode, L.kcode, nullptr, sub, st, false)) != ONEDF_OK) return s;
-    if ((s = do_sort(p, L.kcode, L.scode, L.perm, st)) != ONEDF_OK) return s;
+    if ((s = do_sort(p, L.kcode, L.scode, L.perm, sub, st)) != ONEDF_OK) return s;
     if ((s = do_fwd(p, L.Q, L.K, L.V, L.eps, L.qcode, L.scode, L.perm, L.O, L.idx, L.Z, sub, st, false)) != ONEDF_OK)
         return s;
     if ((s = do_bwd(p, L.Q, L.K, L.V, L.eps, L.O, L.dO, L.idx, L.Z, L.qcode, L.perm, L.dQ, L.dK, L.dV, L.d_eps, sub,

@@ -49,6 +49,7 @@ void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b) {
     b->eps_q = c->take<double>((size_t)total);
     b->eps_part = c->take<double>((size_t)EPS_PARTS);
     b->qorder = c->take<int32_t>((size_t)total);
+    sort_carve(p, c, &b->scr);
 }
 
 struct BwdArgs {
@@ -407,7 +408,7 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     cudaError_t e = cudaSuccess;
     const int32_t* qorder = nullptr;
     if (qcode) {
-        e = launch_query_order(p, qcode, b->qorder, st);
+        e = launch_query_order(p, qcode, b->qorder, b->scr, st);
         if (e != cudaSuccess) return e;
         qorder = b->qorder;
     }

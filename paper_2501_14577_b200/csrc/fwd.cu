@@ -57,6 +57,7 @@ void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f) {
     const int rec = (p->d_k + 1 + 3) / 4 * 4;
     f->recs = c->take<float>((size_t)(BH * p->N * rec));
     f->qorder = c->take<int32_t>((size_t)(BH * p->N));
+    sort_carve(p, c, &f->scr);
 }
 
 // ------------------------------------------------------------------ K4
@@ -523,7 +524,7 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
     ONEDF_DISPATCH_DK(p->d_k, {
         build_records_kernel<DK><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(K, perm, f->recs, N, total);
     });
-    cudaError_t e = launch_query_order(p, qcode, f->qorder, st);
+    cudaError_t e = launch_query_order(p, qcode, f->qorder, f->scr, st);
     if (e != cudaSuccess) return e;
     tr.mark(1, st);
     FwdArgs a;

@@ -19,7 +19,8 @@ struct Trace {
     }
 };
 
-// Longest run the shared-memory segmented sort handles (keys + ping-pong in smem).
+// Longest run the shared-memory segmented sort keeps on chip (keys + ping-pong
+// in smem); longer runs sort through global scratch (SortScratch).
 constexpr int64_t SEG_SORT_MAX = 8192;
 
 int effective_bits(const onedf_problem* p);
@@ -34,9 +35,16 @@ cudaError_t launch_encode(const onedf_problem* p, int b, const float* Q, const f
                           cudaStream_t st);
 
 // sort.cu
+// Global ping-pong scratch of the run sort, only for runs longer than SEG_SORT_MAX (else null).
+struct SortScratch {
+    uint64_t* k[2];
+    uint32_t* v[2];
+};
+void sort_carve(const onedf_problem* p, Carver* c, SortScratch* s);
 cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode /* nullable */,
-                            int32_t* perm, cudaStream_t st);
-cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, int32_t* qorder, cudaStream_t st);
+                            int32_t* perm, const SortScratch& scr, cudaStream_t st);
+cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, int32_t* qorder,
+                               const SortScratch& scr, cudaStream_t st);
 struct TransposeBufs {
     uint32_t* keys[2];
     uint32_t* vals[2];
@@ -66,6 +74,7 @@ cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const 
 struct FwdBufs {
     float* recs;        // [BH][N][RecW] sorted key records
     int32_t* qorder;    // [BH][N] query schedule (per chunk, by qcode)
+    SortScratch scr;    // for the query-order sort of long runs
 };
 void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f);
 cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
@@ -80,6 +89,7 @@ struct BwdBufs {
     double* eps_q;      // [BH][N]    per-query d_eps contribution
     double* eps_part;   // [EPS_PARTS]
     int32_t* qorder;    // [BH][N]    query schedule (when qcode is given)
+    SortScratch scr;    // for the query-order sort of long runs
 };
 void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b);
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,

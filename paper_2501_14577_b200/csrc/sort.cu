@@ -21,26 +21,47 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <type_traits>
+
 namespace onedf {
 
 // ============================================================================ K3
 constexpr int SEG_MAX_WARPS = 16;
+constexpr int SEG_BIG_WARPS = 32;      // runs longer than SEG_SORT_MAX: keys stay in global scratch
 
-__global__ void __launch_bounds__(SEG_MAX_WARPS * 32) seg_sort_kernel(
+// One CTA sorts one run.  SMEM: the run (<= SEG_SORT_MAX keys) lives in shared
+// memory with 16-bit local positions; otherwise the ping-pong key/position
+// buffers are global scratch (same algorithm, L2-resident per run) and only
+// the digit histograms are in shared memory.
+template <bool SMEM>
+__global__ void __launch_bounds__((SMEM ? SEG_MAX_WARPS : SEG_BIG_WARPS) * 32) seg_sort_kernel(
     const uint64_t* __restrict__ kcode, uint64_t* __restrict__ scode, int32_t* __restrict__ perm,
-    int64_t N, int64_t M, int64_t runs_per_bh) {
+    int64_t N, int64_t M, int64_t runs_per_bh, SortScratch scr) {
+    using Pos = typename std::conditional<SMEM, uint16_t, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem[];
     const int64_t bh = blockIdx.x / runs_per_bh;
     const int64_t c = blockIdx.x % runs_per_bh;
     const int64_t s0 = c * M;
     const int n = (int)min64(M, N - s0);
     const int nw = blockDim.x / 32;
-    const int nmax = (int)M;
-    uint64_t* keys0 = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* keys1 = keys0 + nmax;
-    uint16_t* vals0 = reinterpret_cast<uint16_t*>(keys1 + nmax);
-    uint16_t* vals1 = vals0 + nmax;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(vals1 + ((nmax + 7) & ~7));  // [256][nw]
+    uint64_t *keys0, *keys1;
+    Pos *vals0, *vals1;
+    uint32_t* hist;
+    if (SMEM) {
+        const int nmax = (int)M;
+        keys0 = reinterpret_cast<uint64_t*>(smem);
+        keys1 = keys0 + nmax;
+        vals0 = reinterpret_cast<Pos*>(keys1 + nmax);
+        vals1 = vals0 + nmax;
+        hist = reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(vals1) + ((nmax + 7) & ~7));  // [256][nw]
+    } else {
+        const int64_t o = bh * N + s0;
+        keys0 = scr.k[0] + o;
+        keys1 = scr.k[1] + o;
+        vals0 = reinterpret_cast<Pos*>(scr.v[0] + o);
+        vals1 = reinterpret_cast<Pos*>(scr.v[1] + o);
+        hist = reinterpret_cast<uint32_t*>(smem);
+    }
     __shared__ unsigned long long s_and, s_or;
 
     const uint64_t* src = kcode + bh * N + s0;
@@ -48,7 +69,7 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) seg_sort_kernel(
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
         uint64_t k = src[r];
         keys0[r] = k;
-        vals0[r] = (uint16_t)r;
+        vals0[r] = (Pos)r;
         my_and &= k;
         my_or |= k;
     }
@@ -67,7 +88,7 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) seg_sort_kernel(
     const int per_warp = (n + nw - 1) / nw;
     const int w0 = min(n, w * per_warp), w1 = min(n, w0 + per_warp);
     uint64_t* ks = keys0; uint64_t* kd = keys1;
-    uint16_t* vs = vals0; uint16_t* vd = vals1;
+    Pos* vs = vals0; Pos* vd = vals1;
 
     for (int shift = 0; shift < 64; shift += 8) {
         if (((varying >> shift) & 0xffull) == 0) continue;   // uniform across threads
@@ -90,8 +111,7 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) seg_sort_kernel(
             const int a = threadIdx.x * per, b = min(total, a + per);
             uint32_t sum = 0;
             for (int t = a; t < b; ++t) sum += hist[t];
-            // block exclusive scan of per-thread sums
-            __shared__ uint32_t wsum[SEG_MAX_WARPS];
+            __shared__ uint32_t wsum[SEG_BIG_WARPS];
             uint32_t incl = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -124,13 +144,13 @@ __global__ void __launch_bounds__(SEG_MAX_WARPS * 32) seg_sort_kernel(
         }
         __syncthreads();
         uint64_t* tk = ks; ks = kd; kd = tk;
-        uint16_t* tv = vs; vs = vd; vd = tv;
+        Pos* tv = vs; vs = vd; vd = tv;
     }
     uint64_t* outk = scode ? scode + bh * N + s0 : nullptr;
     int32_t* outp = perm + bh * N + s0;
     for (int r = threadIdx.x; r < n; r += blockDim.x) {
         if (scode) outk[r] = ks[r];
-        outp[r] = (int32_t)(s0 + vs[r]);
+        outp[r] = (int32_t)(s0 + (int64_t)vs[r]);
     }
 }
 
@@ -138,17 +158,32 @@ static size_t seg_sort_smem(int64_t M, int nw) {
     return (size_t)M * 8 * 2 + (size_t)((M + 7) & ~7ll) * 2 * 2 + 256 * (size_t)nw * 4;
 }
 
+void sort_carve(const onedf_problem* p, Carver* c, SortScratch* s) {
+    const bool big = run_len_max(p) > SEG_SORT_MAX;
+    const size_t n = big ? (size_t)(p->B * p->H * p->N) : 0;
+    for (int b = 0; b < 2; ++b) {
+        s->k[b] = big ? c->take<uint64_t>(n) : nullptr;
+        s->v[b] = big ? c->take<uint32_t>(n) : nullptr;
+    }
+}
+
 cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode, int32_t* perm,
-                            cudaStream_t st) {
+                            const SortScratch& scr, cudaStream_t st) {
     const int64_t N = p->N, BH = p->B * p->H;
     const int64_t M = run_len_max(p);
     const int64_t runs = num_runs(p);
+    if (M > SEG_SORT_MAX) {
+        const size_t smem = 256 * (size_t)SEG_BIG_WARPS * 4;
+        seg_sort_kernel<false><<<(unsigned)(BH * runs), SEG_BIG_WARPS * 32, smem, st>>>(kcode, scode, perm, N, M,
+                                                                                        runs, scr);
+        return cudaGetLastError();
+    }
     int nw = (int)((M + 32 * 8 - 1) / (32 * 8));   // ~8 keys per lane
     nw = nw < 1 ? 1 : (nw > SEG_MAX_WARPS ? SEG_MAX_WARPS : nw);
     const size_t smem = seg_sort_smem(M, nw);
-    cudaError_t e = cudaFuncSetAttribute(seg_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(seg_sort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    seg_sort_kernel<<<(unsigned)(BH * runs), nw * 32, smem, st>>>(kcode, scode, perm, N, M, runs);
+    seg_sort_kernel<true><<<(unsigned)(BH * runs), nw * 32, smem, st>>>(kcode, scode, perm, N, M, runs, scr);
     return cudaGetLastError();
 }
 
@@ -157,8 +192,9 @@ cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint6
 // schedule slots are then close in space, which is what lets a CTA's warps
 // share candidate records and gathered rows through L1.  Pure reordering of
 // work -- no output depends on it.
-cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, int32_t* qorder, cudaStream_t st) {
-    return launch_seg_sort(p, qcode, nullptr, qorder, st);
+cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, int32_t* qorder,
+                               const SortScratch& scr, cudaStream_t st) {
+    return launch_seg_sort(p, qcode, nullptr, qorder, scr, st);
 }
 
 // ============================================================================ K8

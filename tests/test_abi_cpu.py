@@ -77,10 +77,16 @@ def test_validate_accepts_and_sizes(onedf):
     assert onedf.onedf_workspace_size(p, onedf.OP_BWD) >= 6 * 1000 * 32 * 8
 
 
-def test_run_length_limit_is_unsupported(onedf):
+def test_long_runs_are_supported_with_global_scratch(onedf):
+    """Runs longer than the on-chip sort limit validate and get a sort workspace for the
+    global-scratch path (2 x (8 + 4) bytes per position); short runs need no scratch."""
     kw = dict(GOOD)
-    kw.update(N=4 * onedf.onedf_max_run_length(), chunk=2 * onedf.onedf_max_run_length())
-    assert onedf.onedf_validate(onedf.Problem(*kw.values())) == onedf.abi.ERR_UNSUPPORTED
+    m = onedf.onedf_max_run_length()
+    kw.update(N=4 * m, chunk=2 * m)
+    p = onedf.Problem(*kw.values())
+    assert onedf.onedf_validate(p) == onedf.OK
+    assert onedf.onedf_workspace_size(p, onedf.OP_SORT) >= 24 * p.B * p.H * p.N
+    assert onedf.onedf_workspace_size(onedf.Problem(*GOOD.values()), onedf.OP_SORT) == 256
 
 
 def test_calls_check_arguments_before_any_launch(onedf):

@@ -77,6 +77,9 @@ EDGE = {
     "chunk_gt_N": dict(B=1, H=1, N=50, d_k=3, d_v=8, k=4, window=8, chunk=64, causal=1, mean_slot=1),
     "bits_small": dict(B=1, H=1, N=256, d_k=3, d_v=8, k=8, window=16, chunk=32, bits=3, causal=1, mean_slot=1),
     "seg_8192": dict(B=1, H=1, N=16384, d_k=3, d_v=8, k=8, window=16, chunk=8192, causal=1, mean_slot=1),
+    # runs longer than the on-chip sort limit (global-scratch sort path)
+    "seg_big_causal": dict(B=1, H=2, N=20000, d_k=3, d_v=8, k=8, window=16, chunk=10000, causal=1, mean_slot=1),
+    "seg_big_noncausal": dict(B=1, H=1, N=9000, d_k=2, d_v=8, k=8, window=16, chunk=1, causal=0, mean_slot=1),
 }
 
 
@@ -193,6 +196,31 @@ def test_long64k_bench_config_sampled():
     valid = idx >= 0
     assert np.all(np.where(valid, idx < lim[None, :, None], True))
     assert np.all(valid.sum(-1) == np.minimum(cfg.k, lim)[None, :])
+
+
+@pytest.mark.parametrize("name", ["long512k", "long1m"])
+def test_long_sequence_single_slice_sampled(name):
+    """BASELINE long-sequence scaling shapes (runs of 16K / 32K keys, sorted through global
+    scratch) on one (b,h) slice: codes, runs and permutation bit-exact everywhere, idx/O/Z on
+    sampled queries, gradient invariants."""
+    cfg = synth.CONFIGS[name].with_(B=1, H=1)
+    kw = cfg.problem_kwargs()
+    x = synth.make_inputs(cfg)
+    got = gpu_run(kw, x)
+    p = oracle.Problem(**kw)
+    qc, kc, _ = oracle.encode(p, x["Q"], x["K"])
+    sc, pm = oracle.sort(p, kc)
+    assert_same(got["qcode"], qc, "qcode")
+    assert_same(got["kcode"], kc, "kcode")
+    assert_same(got["scode"], sc, "scode")
+    assert_same(got["perm"], pm, "perm")
+    sel = synth.sample_queries(cfg, 300)
+    idx_ref = oracle.select(p, x["Q"], x["K"], qc, sc, pm, sel=sel)
+    assert_same(got["idx"].reshape(-1, cfg.k)[sel], idx_ref, "idx[sampled]")
+    O_ref, Z_ref = oracle.forward(p, x["Q"], x["K"], x["V"], synth.EPS, idx_ref, sel=sel)
+    assert_close(got["O"].reshape(-1, cfg.d_v)[sel], O_ref, "O[sampled]")
+    assert_close(got["Z"].reshape(-1)[sel], Z_ref, "Z[sampled]")
+    _gradient_invariants(kw, x, got)
 
 
 def test_determinism_bitwise():
