@@ -47,6 +47,12 @@ constexpr int FWD_THREADS = FWD_WARPS * 32;
 #ifndef ONEDF_FWD_MINB
 #define ONEDF_FWD_MINB 4
 #endif
+#ifndef ONEDF_FWD_COLLECT
+#define ONEDF_FWD_COLLECT 1          // pass-2 append: 0 ballot + popc compaction, 1 shared-memory atomic cursor
+#endif
+#ifndef ONEDF_FWD_RANK
+#define ONEDF_FWD_RANK 0             // order of the collected keys: 0 rank counting, 1 register bitonic sort
+#endif
 constexpr int FWD_QPW = ONEDF_FWD_QPW;              // queries per warp (schedule stretch per CTA = 8*QPW)
 constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 loaded ahead (W = 128 -> one window)
 constexpr int FWD_CAP = 256;                        // pass-2 collection capacity per warp
@@ -140,6 +146,55 @@ __device__ __forceinline__ unsigned long long list_get(const unsigned long long 
     for (int r = 1; r < R; ++r) v = (e >> 5) == r ? top[r] : v;
     return __shfl_sync(FULL, v, e & 31);
 }
+
+// Ascending bitonic sort of 32*R keys spread over the warp (element e = r*32 + lane).
+template <int R>
+__device__ __forceinline__ void warp_sort(unsigned long long (&x)[R]) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+                const int rs = stride / 32;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if ((r & rs) == 0) {
+                        const bool up = ((r * 32) & size) == 0;
+                        const unsigned long long a = x[r], b = x[r + rs];
+                        const unsigned long long lo = umin64(a, b), hi = umax64(a, b);
+                        x[r] = up ? lo : hi;
+                        x[r + rs] = up ? hi : lo;
+                    }
+                }
+            } else {
+                const bool lower = (lane & stride) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const bool up = size >= 32 ? ((r * 32) & size) == 0 : (lane & size) == 0;
+                    const unsigned long long y = __shfl_xor_sync(FULL, x[r], stride);
+                    x[r] = (lower == up) ? umin64(x[r], y) : umax64(x[r], y);
+                }
+            }
+        }
+    }
+}
+
+// The first 32*RO keys (ascending) of buf[0..cnt) (unique keys), sorted as 32*RS.
+template <int RS, int RO>
+__device__ __forceinline__ void sort_collected(const unsigned long long* buf, int cnt, unsigned long long (&top)[RO]) {
+    const int lane = lane_id();
+    unsigned long long x[RS];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) x[r] = r * 32 + lane < cnt ? buf[r * 32 + lane] : KEY_MAX;
+    warp_sort<RS>(x);
+#pragma unroll
+    for (int r = 0; r < RO; ++r) top[r] = r < RS ? x[r] : KEY_MAX;
+}
+
+#ifdef ONEDF_FWD_STATS
+__device__ unsigned long long g_fwd_stats[8];
+#endif
 
 struct FwdArgs {
     const float* Q; const float* K; const float* V; const float* eps;
@@ -256,6 +311,7 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
     constexpr int L = PassOne<R>::L;
     __shared__ __align__(16) unsigned long long s_buf[FWD_WARPS][FWD_CAP + 32 * FWD_UB];
     __shared__ __align__(16) unsigned long long s_top[FWD_WARPS][32 * R];
+    __shared__ int s_cnt[FWD_WARPS];
     const int warp = threadIdx.x / 32, lane = lane_id();
     unsigned long long* buf = s_buf[warp];
     unsigned long long* stop = s_top[warp];
@@ -339,6 +395,24 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         // ---------------- A6 pass 2: collect every candidate with D <= T (order is
         // irrelevant: the final order comes from ranking the unique keys)
         int cnt = 0;
+#if ONEDF_FWD_COLLECT == 1
+        if (lane == 0) s_cnt[warp] = 0;
+        __syncwarp();
+        cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB], const bool (&ok)[FWD_UB], int,
+                                int) {
+#pragma unroll
+            for (int uu = 0; uu < FWD_UB; ++uu) {
+                if (ok[uu] && __float_as_uint(D[uu]) <= tb) {
+                    const int pos = atomicAdd(&s_cnt[warp], 1);
+                    if (pos < FWD_CAP) buf[pos] = make_key(D[uu], jj[uu]);
+                }
+            }
+            return true;
+        });
+        __syncwarp();
+        cnt = s_cnt[warp];
+        const bool fits = cnt <= FWD_CAP;
+#else
         const bool fits = cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB],
                                                   const bool (&ok)[FWD_UB], int, int) {
 #pragma unroll
@@ -350,8 +424,25 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
             }
             return cnt <= FWD_CAP;                     // buf has FWD_CAP + 32*FWD_UB slots
         });
+#endif
+#ifdef ONEDF_FWD_STATS
+        if (lane == 0) {
+            atomicAdd(&g_fwd_stats[0], 1ull);
+            atomicAdd(&g_fwd_stats[1], (unsigned long long)cnt);
+            atomicAdd(&g_fwd_stats[2], (unsigned long long)cnt * cnt);
+            atomicAdd(&g_fwd_stats[3], fits ? 0ull : 1ull);
+        }
+#endif
         __syncwarp();
+        unsigned long long top[R];
         if (fits) {
+#if ONEDF_FWD_RANK == 1
+            // ---------------- exact order of the collected keys: register bitonic sort
+            if (cnt <= 32 * R) sort_collected<R, R>(buf, cnt, top);
+            else if (cnt <= 64 * R) sort_collected<(2 * R > 8 ? 8 : 2 * R), R>(buf, cnt, top);
+            else if (cnt <= 128 * R || R >= 4) sort_collected<(4 * R > 8 ? 8 : 4 * R), R>(buf, cnt, top);
+            else sort_collected<8, R>(buf, cnt, top);
+#else
             // ---------------- exact order of the collected keys by counting (keys are unique)
             for (int t = lane; t < 32 * R; t += 32) stop[t] = KEY_MAX;
             __syncwarp();
@@ -370,11 +461,14 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
                 for (; x < cnt; ++x) rank += buf[x] < mine;
                 if (e2 < cnt && rank < k) stop[rank] = mine;
             }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < R; ++r) top[r] = stop[r * 32 + lane];
+#endif
         } else {
             // ---------------- rare: too many keys at or below T (e.g. many equal
             // distances) -- streaming selection with shuffle-bitonic merges,
             // starting from the same bound
-            unsigned long long top[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) top[r] = KEY_MAX;
             unsigned long long thresh = tb >= 0x7f800000u ? KEY_MAX : ((unsigned long long)(tb + 1u) << 32);
@@ -408,13 +502,7 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
                 __syncwarp();
                 merge_pending<R>(top, lane < pc ? pend[lane] : KEY_MAX);
             }
-#pragma unroll
-            for (int r = 0; r < R; ++r) stop[r * 32 + lane] = top[r];
         }
-        __syncwarp();
-        unsigned long long top[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) top[r] = stop[r * 32 + lane];
         __syncwarp();   // buf/stop are rewritten by the next query
 
         // ---------------- outputs: idx row (slot e = r*32 + lane), valid count
@@ -548,3 +636,14 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
 }
 
 }  // namespace onedf
+
+#ifdef ONEDF_FWD_STATS
+// tools only (variant builds): [queries, sum cnt, sum cnt^2, fallbacks], then reset
+extern "C" int onedf_debug_fwd_stats(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, onedf::g_fwd_stats, 8 * sizeof(unsigned long long));
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(onedf::g_fwd_stats, z, sizeof(z));
+    return 0;
+}
+#endif

@@ -39,5 +39,16 @@ for _ in range(a.reps + 1):
     torch.cuda.synchronize()
     ts.append((e0.elapsed_time(e1), e1.elapsed_time(e2)))
 ts = ts[1:]
+try:
+    import ctypes
+    from paper_2501_14577_b200 import abi as _abi
+    st = (ctypes.c_ulonglong * 8)()
+    _abi._lib.onedf_debug_fwd_stats(st)
+    n = st[0]
+    if n:
+        mean = st[1] / n
+        print(f"fwd stats: queries {n}  mean cnt {mean:.1f}  rms {(st[2] / n) ** 0.5:.1f}  fallbacks {st[3]}")
+except AttributeError:
+    pass
 print(f"{os.environ.get('ONEDF_LIB', 'default')}: fwd {min(t[0] for t in ts):.2f} ms  bwd {min(t[1] for t in ts):.2f} ms"
       f"  idxsum {int(idx.sum())} Osum {float(O.double().sum()):.6f}")
