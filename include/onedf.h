@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define ONEDF_VERSION 200
+#define ONEDF_VERSION 300
 
 typedef struct CUstream_st* onedf_stream_t;   /* == cudaStream_t */
 
@@ -76,6 +76,8 @@ typedef struct {
     int32_t bits;        /* b : bits per dim, d_k*b <= 63, b <= 32; 0 -> min(63/d_k,32) */
     int32_t causal;      /* 1: key j visible to query i iff j < floor(i/M)*M (D6); 0: all */
     int32_t mean_slot;   /* 1: append the prefix-mean token (D8); 0: off      */
+    int32_t shard_rank;  /* sequence sharding (NEXT-1, see "Sequence sharding" below): */
+    int32_t shard_world; /*   this rank of shard_world; shard_world 0 or 1 = unsharded  */
 } onedf_problem;
 
 enum {
@@ -185,6 +187,55 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
                                        float* O_h, float* dQ_h, float* dK_h, float* dV_h,
                                        double* d_eps_h, void* ws, size_t ws_bytes,
                                        onedf_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * Sequence sharding (north_star "sequence sharding, with
+ * an NCCL all-gather over NVLink of the earlier ranks' sorted Morton runs").
+ * Causal problems only (shard_world > 1 with causal == 0 -> UNSUPPORTED).
+ * The C = ceil(N/M) chunks of every (b,h) are dealt zig-zag over the
+ * shard_world ranks: chunk c belongs to rank onedf_shard_owner(c, world)
+ * (g = c mod 2*world; owner = g < world ? g : 2*world-1-g), so the causal work
+ * (proportional to c) balances.  Every rank keeps FULL-LENGTH
+ * [B,H,N,.] buffers; a rank "owns" the rows of its chunks:
+ *   onedf_bounds_partial   raw per-dim min/max over the owned rows of Q and K;
+ *                          the caller all-reduces them (MIN over lo, MAX over
+ *                          hi), then onedf_bounds_finish applies D10 and the
+ *                          result is onedf_encode's lohi_in (required).
+ *   onedf_encode/_sort     as unsharded; only owned rows/runs are meaningful.
+ *                          The caller then all-gathers the owned runs of
+ *                          scode/perm and the owned rows of K and V, so that
+ *                          scode, perm, K, V are complete on every rank.
+ *   onedf_topk_attn_fwd    computes O, idx, Z of the OWNED queries only
+ *                          (other rows are not written).
+ *   onedf_topk_attn_bwd    dQ of the owned queries; dK, dV and d_eps are this
+ *                          rank's PARTIAL sums over its owned queries (all N
+ *                          rows written); the caller exchanges the partial rows
+ *                          to their owners and sums them in rank order with
+ *                          onedf_rank_sum (deterministic), and sums d_eps in
+ *                          rank order.
+ * Non-owned rows of Q and dO must hold finite values (e.g. zeros); they are
+ * never read into a result but pass through the mean-slot scans with a zero
+ * coefficient. */
+int32_t onedf_shard_owner(int64_t chunk, int32_t world);
+
+/* Raw min (lohi[...,0,:]) and max (lohi[...,1,:]) per (b,h) per dim over the
+ * owned rows of Q and K (all rows if unsharded); no widening.  lohi: device
+ * double [B,H,2,d_k], overwritten.  Non-finite input -> NONFINITE flag.
+ * Workspace: onedf_workspace_size(p, ONEDF_OP_ENCODE). */
+onedf_status onedf_bounds_partial(const onedf_problem* p, const float* Q, const float* K,
+                                  double* lohi, void* ws, size_t ws_bytes, onedf_stream_t stream);
+
+/* D10 in place: a dim with hi == lo becomes [lo - 0.5, hi + 0.5]; non-finite
+ * or hi < lo -> NONFINITE flag.  onedf_encode(lohi_in = NULL) is exactly
+ * bounds_partial -> bounds_finish -> encode(lohi_in). */
+onedf_status onedf_bounds_finish(const onedf_problem* p, double* lohi, void* ws, size_t ws_bytes,
+                                 onedf_stream_t stream);
+
+/* out[x] = (float) sum_{r = 0 .. world-1} (double) parts[r*n + x], summed in
+ * rank order r = 0, 1, ... (the fixed-order combine of the sharded dK/dV
+ * partials).  parts: device float [world][n]; out: device float [n]. */
+onedf_status onedf_rank_sum(const float* parts, int64_t n, int32_t world, float* out,
+                            onedf_stream_t stream);
 
 /* Synchronises `stream`, then reads the flag word of `ws` (a workspace
  * previously passed to encode/fwd/bwd): ONEDF_OK or ONEDF_ERR_NONFINITE. */

@@ -9,7 +9,8 @@ from .abi import (OK, OP_BWD, OP_ENCODE, OP_FWD, OP_SORT, OP_STEP_HOST, OnedfErr
                   onedf_check_device_status, onedf_encode, onedf_max_run_length, onedf_sort,
                   onedf_topk_attn_bwd, onedf_topk_attn_fwd, onedf_topk_attn_step_host, onedf_validate,
                   onedf_version, onedf_workspace_size, status_string)
-from .api import (HostStep, Workspace, ZetaTopkAttention, check_device_status, default_chunk,  # noqa: F401
-                  encode, make_problem, sort, topk_attn_bwd, topk_attn_fwd, zeta_attention)
+from .api import (HostStep, Workspace, ZetaTopkAttention, bounds_finish, bounds_partial,  # noqa: F401
+                  check_device_status, default_chunk, encode, make_problem, rank_sum, sort, topk_attn_bwd,
+                  topk_attn_fwd, zeta_attention)
 
 __version__ = "0.1.0"

@@ -31,7 +31,8 @@ class Problem(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int64), ("H", ctypes.c_int64), ("N", ctypes.c_int64),
                 ("d_k", ctypes.c_int32), ("d_v", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("window", ctypes.c_int32), ("chunk", ctypes.c_int32), ("bits", ctypes.c_int32),
-                ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32)]
+                ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32),
+                ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32)]
 
     def __repr__(self):
         return "Problem(" + ", ".join(f"{n}={getattr(self, n)}" for n, _ in self._fields_) + ")"
@@ -63,6 +64,10 @@ def _load():
         "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp,
                                              i32, vp]),
         "onedf_topk_attn_step_host": (i32, [P, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_shard_owner": (ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32]),
+        "onedf_bounds_partial": (i32, [P, vp, vp, vp, vp, sz, vp]),
+        "onedf_bounds_finish": (i32, [P, vp, vp, sz, vp]),
+        "onedf_rank_sum": (i32, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp]),
         "onedf_check_device_status": (i32, [vp, vp]),
         "onedf_status_string": (ctypes.c_char_p, [i32]),
         "onedf_version": (i32, []),
@@ -78,6 +83,7 @@ _lib = _load()
 EXPORTS = ("onedf_validate", "onedf_max_run_length", "onedf_workspace_size", "onedf_encode", "onedf_sort",
            "onedf_topk_attn_fwd", "onedf_topk_attn_bwd", "onedf_topk_attn_fwd_traced",
            "onedf_topk_attn_bwd_traced", "onedf_topk_attn_step_host",
+           "onedf_shard_owner", "onedf_bounds_partial", "onedf_bounds_finish", "onedf_rank_sum",
            "onedf_check_device_status", "onedf_status_string", "onedf_version")
 
 
@@ -172,6 +178,24 @@ def onedf_topk_attn_step_host(p, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_
                                           _p(dQ_h), _p(dK_h), _p(dV_h), _p(d_eps_h), _p(ws), ws_bytes,
                                           _stream(stream)),
            "onedf_topk_attn_step_host")
+
+
+def onedf_shard_owner(chunk: int, world: int) -> int:
+    return _lib.onedf_shard_owner(chunk, world)
+
+
+def onedf_bounds_partial(p, Q, K, lohi, ws, ws_bytes, stream=None):
+    _check(_lib.onedf_bounds_partial(ctypes.byref(p), _p(Q), _p(K), _p(lohi), _p(ws), ws_bytes, _stream(stream)),
+           "onedf_bounds_partial")
+
+
+def onedf_bounds_finish(p, lohi, ws, ws_bytes, stream=None):
+    _check(_lib.onedf_bounds_finish(ctypes.byref(p), _p(lohi), _p(ws), ws_bytes, _stream(stream)),
+           "onedf_bounds_finish")
+
+
+def onedf_rank_sum(parts, n: int, world: int, out, stream=None):
+    _check(_lib.onedf_rank_sum(_p(parts), n, world, _p(out), _stream(stream)), "onedf_rank_sum")
 
 
 def onedf_check_device_status(ws, stream=None) -> int:

@@ -10,8 +10,9 @@ from . import abi
 from .abi import Problem
 
 
-def make_problem(B, H, N, d_k, d_v, k, window=0, chunk=1, bits=0, causal=1, mean_slot=1) -> Problem:
-    p = Problem(B, H, N, d_k, d_v, k, window, chunk, bits, causal, mean_slot)
+def make_problem(B, H, N, d_k, d_v, k, window=0, chunk=1, bits=0, causal=1, mean_slot=1, shard_rank=0,
+                 shard_world=1) -> Problem:
+    p = Problem(B, H, N, d_k, d_v, k, window, chunk, bits, causal, mean_slot, shard_rank, shard_world)
     st = abi.onedf_validate(p)
     if st != abi.OK:
         raise abi.OnedfError(st, "onedf_validate")
@@ -62,6 +63,31 @@ def encode(p: Problem, Q, K, lohi=None, ws: Workspace | None = None):
     ptr, n = _ws(p, abi.OP_ENCODE, ws)
     abi.onedf_encode(p, Q, K, None if lohi is None else _dev(lohi, torch.float64), qcode, kcode, lohi_out, ptr, n)
     return qcode, kcode, lohi_out
+
+
+def bounds_partial(p: Problem, Q, K, ws: Workspace | None = None):
+    """Raw per-(b,h) per-dim min/max over the rows this rank owns -> lohi [B,H,2,d_k] f64 (no widening)."""
+    Q, K = _dev(Q), _dev(K)
+    lohi = torch.empty((p.B, p.H, 2, p.d_k), dtype=torch.float64, device=Q.device)
+    ptr, n = _ws(p, abi.OP_ENCODE, ws)
+    abi.onedf_bounds_partial(p, Q, K, lohi, ptr, n)
+    return lohi
+
+
+def bounds_finish(p: Problem, lohi, ws: Workspace | None = None):
+    """Reading D10 in place (hi == lo -> +-0.5); returns lohi."""
+    lohi = _dev(lohi, torch.float64)
+    ptr, n = _ws(p, abi.OP_ENCODE, ws)
+    abi.onedf_bounds_finish(p, lohi, ptr, n)
+    return lohi
+
+
+def rank_sum(parts):
+    """parts [world, ...] f32 -> [...] f32, summed in rank order in f64 (onedf_rank_sum)."""
+    parts = _dev(parts)
+    out = torch.empty(parts.shape[1:], dtype=torch.float32, device=parts.device)
+    abi.onedf_rank_sum(parts, out.numel(), parts.shape[0], out)
+    return out
 
 
 def sort(p: Problem, kcode, ws: Workspace | None = None):

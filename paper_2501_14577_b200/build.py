@@ -37,6 +37,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     """defines/lib/objdir: variant builds for tools/ experiments (the product is the default)."""
     os.makedirs(objdir, exist_ok=True)
     hdrs = _headers()
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    if not force and not defines and not _stale(lib, srcs + hdrs):
+        return lib          # the library is newer than every source (objects need not be present)
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)

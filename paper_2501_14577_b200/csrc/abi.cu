@@ -18,6 +18,16 @@ int64_t run_len_max(const onedf_problem* p) {
     return p->chunk < p->N ? p->chunk : p->N;
 }
 int64_t num_runs(const onedf_problem* p) { return p->causal ? (p->N + p->chunk - 1) / p->chunk : 1; }
+Shard make_shard(const onedf_problem* p) {
+    Shard s;
+    if (p->shard_world > 1) {
+        s.rank = p->shard_rank;
+        s.world = p->shard_world;
+        s.M = run_len_max(p);
+        s.C = num_runs(p);
+    }
+    return s;
+}
 
 static onedf_status check_device() {
     int dev = 0, major = 0, minor = 0;
@@ -46,6 +56,13 @@ static onedf_status validate(const onedf_problem* p) {
     const int b = effective_bits(p);
     if (b < 1 || b > 32 || p->d_k * b > 63) return ONEDF_ERR_INVALID_ARG;
     if (p->N * (int64_t)p->k >= (1ll << 31)) return ONEDF_ERR_INVALID_ARG;
+    if (p->shard_world < 0 || p->shard_world > 4096) return ONEDF_ERR_INVALID_ARG;
+    if (p->shard_world > 1) {
+        if (p->shard_rank < 0 || p->shard_rank >= p->shard_world) return ONEDF_ERR_INVALID_ARG;
+        if (!p->causal) return ONEDF_ERR_UNSUPPORTED;   // sequence sharding is defined over causal chunks
+    } else if (p->shard_rank != 0) {
+        return ONEDF_ERR_INVALID_ARG;
+    }
     return ONEDF_OK;
 }
 
@@ -189,6 +206,8 @@ size_t onedf_workspace_size(const onedf_problem* p, int op) {
 onedf_status onedf_encode(const onedf_problem* p, const float* Q, const float* K, const double* lohi_in,
                           uint64_t* qcode, uint64_t* kcode, double* lohi_out, void* ws, size_t ws_bytes,
                           onedf_stream_t stream) {
+    if (validate(p) == ONEDF_OK && p->shard_world > 1 && !lohi_in)
+        return ONEDF_ERR_INVALID_ARG;   // sharded FIT: bounds_partial + all-reduce + bounds_finish
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_ENCODE);
     if (s != ONEDF_OK) return s;
     if (!Q || !K || !qcode || !kcode) return ONEDF_ERR_INVALID_ARG;
@@ -261,6 +280,7 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
                                        float eps, const float* dO_h, float* O_h, float* dQ_h, float* dK_h,
                                        float* dV_h, double* d_eps_h, void* ws, size_t ws_bytes,
                                        onedf_stream_t stream) {
+    if (validate(p) == ONEDF_OK && p->shard_world > 1) return ONEDF_ERR_UNSUPPORTED;   // needs the caller's collectives
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_STEP_HOST);
     if (s != ONEDF_OK) return s;
     if (!Q_h || !K_h || !V_h || !dO_h || !O_h || !dQ_h || !dK_h || !dV_h || !d_eps_h) return ONEDF_ERR_INVALID_ARG;
@@ -296,6 +316,39 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
     if (e == cudaSuccess) e = cudaMemcpyAsync(dV_h, L.dV, bv, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_eps_h, L.d_eps, 8, cudaMemcpyDeviceToHost, st);
     return finish(e);
+}
+
+int32_t onedf_shard_owner(int64_t chunk, int32_t world) {
+    if (world <= 1 || chunk < 0) return 0;
+    return Shard::owner(chunk, world);
+}
+
+onedf_status onedf_bounds_partial(const onedf_problem* p, const float* Q, const float* K, double* lohi, void* ws,
+                                  size_t ws_bytes, onedf_stream_t stream) {
+    onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_ENCODE);
+    if (s != ONEDF_OK) return s;
+    if (!Q || !K || !lohi) return ONEDF_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+    Carver c(ws);
+    return finish(launch_bounds_partial(p, Q, K, lohi, ws, &c, st));
+}
+
+onedf_status onedf_bounds_finish(const onedf_problem* p, double* lohi, void* ws, size_t ws_bytes,
+                                 onedf_stream_t stream) {
+    onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_ENCODE);
+    if (s != ONEDF_OK) return s;
+    if (!lohi) return ONEDF_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+    return finish(launch_bounds_finish(p, lohi, ws, st));
+}
+
+onedf_status onedf_rank_sum(const float* parts, int64_t n, int32_t world, float* out, onedf_stream_t stream) {
+    if (!parts || !out || n < 0 || world < 1) return ONEDF_ERR_INVALID_ARG;
+    onedf_status s = check_device();
+    if (s != ONEDF_OK) return s;
+    return finish(launch_rank_sum(parts, n, world, out, (cudaStream_t)stream));
 }
 
 onedf_status onedf_check_device_status(const void* ws, onedf_stream_t stream) {

@@ -57,8 +57,9 @@ struct BwdArgs {
     const float* O; const float* dO; const int32_t* idx; const float* Z;
     const float* Kbar; const float* Vbar; const int32_t* qorder;
     float* dQ; float2* coeff; float2* muco; double* eps_q;
-    int64_t N, total;
+    int64_t N, total, nq;        // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
     int k, dv, causal, mean_slot;
+    Shard sh;
     void* ws;
 };
 
@@ -99,8 +100,10 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
     const int64_t slot = (int64_t)blockIdx.x * BWD_WARPS + warp;
     if (slot >= a.total) return;
     const int64_t N = a.N;
-    const int64_t bh = slot / N;
-    const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + slot) : slot % N;
+    const int64_t bh = slot / a.nq;
+    int64_t pos;
+    if (!a.sh.slot_pos(slot - bh * a.nq, N, pos)) return;      // sharded: padding of a short last chunk
+    const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + bh * N + pos) : pos;
     const int64_t gq = bh * N + i;
     const float e = __ldg(a.eps);
     if (slot == 0 && lane == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
@@ -416,16 +419,26 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.O = O; a.dO = dO; a.idx = idx; a.Z = Z;
     a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.qorder = qorder;
     a.dQ = dQ; a.coeff = b->coeff; a.muco = b->muco; a.eps_q = b->eps_q;
-    a.N = N; a.total = total; a.k = p->k; a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
+    a.sh = make_shard(p);
+    a.nq = a.sh.slots(N);
+    a.N = N; a.total = BH * a.nq; a.k = p->k; a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
     a.ws = ws;
+    if (a.sh.on()) {
+        // rows of queries this rank does not own stay zero: they enter the A11 scan and the eps sum
+        e = cudaMemsetAsync(b->muco, 0, (size_t)total * sizeof(float2), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(b->eps_q, 0, (size_t)total * sizeof(double), st);
+        if (e != cudaSuccess) return e;
+    }
     const int P = lanes_per_row(p->d_v);
-    const unsigned qgrid = (unsigned)((total + BWD_WARPS - 1) / BWD_WARPS);
+    const unsigned qgrid = (unsigned)((a.total + BWD_WARPS - 1) / BWD_WARPS);
+    const unsigned kgrid = (unsigned)((total + BWD_WARPS - 1) / BWD_WARPS);
 #define ONEDF_BWDQR(PV, RV)                                                                            \
     ONEDF_DISPATCH_DK(p->d_k, {                                                                        \
         if constexpr (PV == 32) {                                                                      \
-            if (p->d_v > 128) bwd_query_kernel<DK, PV, 2, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);        \
+            if (!qgrid) {}                                                                            \
+            else if (p->d_v > 128) bwd_query_kernel<DK, PV, 2, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);  \
             else bwd_query_kernel<DK, PV, 1, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);                    \
-        } else {                                                                                       \
+        } else if (qgrid) {                                                                            \
             bwd_query_kernel<DK, PV, 1, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);                         \
         }                                                                                              \
     })
@@ -451,10 +464,10 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
 #define ONEDF_BWDK(PV)                                                                                 \
     ONEDF_DISPATCH_DK(p->d_k, {                                                                        \
         if constexpr (PV == 32) {                                                                      \
-            if (p->d_v > 128) bwd_key_kernel<DK, PV, 2><<<qgrid, BWD_THREADS, 0, st>>>(ka);            \
-            else bwd_key_kernel<DK, PV, 1><<<qgrid, BWD_THREADS, 0, st>>>(ka);                         \
+            if (p->d_v > 128) bwd_key_kernel<DK, PV, 2><<<kgrid, BWD_THREADS, 0, st>>>(ka);            \
+            else bwd_key_kernel<DK, PV, 1><<<kgrid, BWD_THREADS, 0, st>>>(ka);                         \
         } else {                                                                                       \
-            bwd_key_kernel<DK, PV, 1><<<qgrid, BWD_THREADS, 0, st>>>(ka);                              \
+            bwd_key_kernel<DK, PV, 1><<<kgrid, BWD_THREADS, 0, st>>>(ka);                              \
         }                                                                                              \
     })
     if (P == 4) { ONEDF_BWDK(4) }

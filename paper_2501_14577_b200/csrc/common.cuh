@@ -85,6 +85,40 @@ __device__ __forceinline__ double dist64(const float* q, const float* k) {
     return acc;
 }
 
+// Sequence sharding (onedf.h "Sequence sharding"): chunk c of every (b,h)
+// belongs to rank owner(c) (zig-zag over 2*world); a rank computes the
+// queries of its chunks.  world <= 1: everything is owned.
+struct Shard {
+    int32_t rank = 0, world = 1;
+    int64_t M = 1, C = 1;          // chunk length, chunks per (b,h)
+    __host__ __device__ static int32_t owner(int64_t c, int32_t world) {
+        const int64_t g = c % (2 * (int64_t)world);
+        return (int32_t)(g < world ? g : 2 * (int64_t)world - 1 - g);
+    }
+    __host__ __device__ bool on() const { return world > 1; }
+    __host__ __device__ bool owns_row(int64_t i) const { return world <= 1 || owner(i / M, world) == rank; }
+    // t-th owned chunk in ascending order
+    __host__ __device__ int64_t chunk_of(int64_t t) const {
+        const int64_t P2 = 2 * (int64_t)world;
+        return P2 * (t / 2) + ((t & 1) ? P2 - 1 - rank : rank);
+    }
+    __host__ int64_t n_owned() const {
+        if (world <= 1) return C;
+        int64_t t = 0;
+        while (chunk_of(t) < C) ++t;
+        return t;
+    }
+    // query-schedule slots per (b,h): all N, or the owned chunks padded to M
+    __host__ int64_t slots(int64_t N) const { return world <= 1 ? N : n_owned() * M; }
+    // slot s of a (b,h) -> schedule position (chunk-major); false for padding
+    __device__ __forceinline__ bool slot_pos(int64_t s, int64_t N, int64_t& pos) const {
+        if (world <= 1) { pos = s; return true; }
+        const int64_t t = s / M;
+        pos = chunk_of(t) * M + (s - t * M);
+        return pos < N;
+    }
+};
+
 __device__ __forceinline__ void set_flag(void* ws, unsigned bit) {
     atomicOr((unsigned*)ws, bit);
 }

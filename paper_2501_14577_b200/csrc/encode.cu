@@ -45,7 +45,7 @@ __device__ __forceinline__ void load_rows4(const float* __restrict__ X, int64_t 
 template <int DK>
 __global__ void __launch_bounds__(ENC_THREADS) bounds_partial_kernel(
     const float* __restrict__ Q, const float* __restrict__ K, int64_t N, int splits, bool vec_ok,
-    float* __restrict__ part /* [BH][splits][2][DK] */, void* ws) {
+    float* __restrict__ part /* [BH][splits][2][DK] */, void* ws, Shard sh) {
     const int s = blockIdx.x;
     const int64_t bh = blockIdx.y;
     const int64_t groups = (N + ENC_ROWS - 1) / ENC_ROWS;
@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(ENC_THREADS) bounds_partial_kernel(
 #pragma unroll
             for (int r = 0; r < ENC_ROWS; ++r) {
                 if (r >= nrows) break;
+                if (sh.on() && !sh.owns_row(g * ENC_ROWS + r)) continue;   // sharded: owned rows only
 #pragma unroll
                 for (int d = 0; d < DK; ++d) {
                     float v = x[r][d];
@@ -229,10 +230,75 @@ cudaError_t launch_encode(const onedf_problem* p, int b, const float* Q, const f
     ONEDF_DISPATCH_DK(p->d_k, {
         // always run: with caller-fixed bounds it is the finiteness check
         bounds_partial_kernel<DK><<<dim3(splits, (unsigned)BH), ENC_THREADS, 0, st>>>(Q, K, N, splits, vec_ok, part,
-                                                                                      ws);
+                                                                                      ws, make_shard(p));
         encode_kernel<DK><<<egrid, ENC_THREADS, 0, st>>>(Q, K, N, b, vec_ok, part, splits, lohi_in, qcode, kcode,
                                                          lohi_out, ws);
     });
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- bounds-only entry points
+// raw per-(b,h) per-dim min/max from the split partials (no widening)
+__global__ void bounds_reduce_kernel(const float* __restrict__ part, int splits, int dk, double* __restrict__ lohi) {
+    const int64_t bh = blockIdx.x;
+    const int d = threadIdx.x;
+    if (d >= dk) return;
+    float a = INFINITY, c = -INFINITY;
+    for (int s = 0; s < splits; ++s) {
+        const float* pp = part + ((bh * splits + s) * 2) * dk;
+        a = fminf(a, pp[d]);
+        c = fmaxf(c, pp[dk + d]);
+    }
+    lohi[bh * 2 * dk + d] = a;
+    lohi[bh * 2 * dk + dk + d] = c;
+}
+
+// D10: hi == lo widens by +-0.5 (the same rule encode_kernel applies when fitting)
+__global__ void bounds_finish_kernel(double* __restrict__ lohi, int64_t BH, int dk, void* ws) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= BH * dk) return;
+    const int64_t bh = t / dk;
+    const int d = (int)(t % dk);
+    double lo = lohi[bh * 2 * dk + d], hi = lohi[bh * 2 * dk + dk + d];
+    if (hi == lo) { lo -= 0.5; hi += 0.5; }
+    if (!isfinite(lo) || !isfinite(hi) || !(hi > lo)) set_flag(ws, FLAG_NONFINITE_INPUT);
+    lohi[bh * 2 * dk + d] = lo;
+    lohi[bh * 2 * dk + dk + d] = hi;
+}
+
+cudaError_t launch_bounds_partial(const onedf_problem* p, const float* Q, const float* K, double* lohi, void* ws,
+                                  Carver* c, cudaStream_t st) {
+    const int64_t BH = p->B * p->H, N = p->N;
+    const int splits = bounds_splits(N, BH);
+    float* part = c->take<float>((size_t)BH * splits * 2 * p->d_k);
+    const bool vec_ok = ((N * p->d_k) % 4 == 0) && ((((uintptr_t)Q) | ((uintptr_t)K)) & 15) == 0;
+    ONEDF_DISPATCH_DK(p->d_k, {
+        bounds_partial_kernel<DK><<<dim3(splits, (unsigned)BH), ENC_THREADS, 0, st>>>(Q, K, N, splits, vec_ok, part,
+                                                                                      ws, make_shard(p));
+    });
+    bounds_reduce_kernel<<<(unsigned)BH, 32, 0, st>>>(part, splits, p->d_k, lohi);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bounds_finish(const onedf_problem* p, double* lohi, void* ws, cudaStream_t st) {
+    const int64_t n = p->B * p->H * p->d_k;
+    bounds_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lohi, p->B * p->H, p->d_k, ws);
+    return cudaGetLastError();
+}
+
+// Fixed-order combine of per-rank partials: f64 sum in rank order, one f32 rounding.
+__global__ void rank_sum_kernel(const float* __restrict__ parts, int64_t n, int32_t world, float* __restrict__ out) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int32_t r = 0; r < world; ++r) acc += (double)__ldg(parts + (int64_t)r * n + x);
+        out[x] = (float)acc;
+    }
+}
+
+cudaError_t launch_rank_sum(const float* parts, int64_t n, int32_t world, float* out, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t blocks = min64((n + 255) / 256, 148 * 16);
+    rank_sum_kernel<<<(unsigned)blocks, 256, 0, st>>>(parts, n, world, out);
     return cudaGetLastError();
 }
 

@@ -201,8 +201,9 @@ struct FwdArgs {
     const uint64_t* qcode; const uint64_t* scode; const float* recs; const int32_t* qorder;
     const float* Kbar; const float* Vbar;
     float* O; int32_t* idx; float* Z;
-    int64_t N, M, total;
+    int64_t N, M, total, nq;     // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
     int k, W, dv, causal, mean_slot;
+    Shard sh;
     void* ws;
 };
 
@@ -325,8 +326,10 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
     for (int u = 0; u < FWD_QPW; ++u) {
         const int64_t slot = ((int64_t)blockIdx.x * FWD_QPW + u) * FWD_WARPS + warp;
         if (slot >= a.total) break;
-        const int64_t bh = slot / N;
-        const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + slot) : slot % N;
+        const int64_t bh = slot / a.nq;
+        int64_t pos;
+        if (!a.sh.slot_pos(slot - bh * a.nq, N, pos)) continue;     // sharded: padding of a short last chunk
+        const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + bh * N + pos) : pos;
         const int64_t gq = bh * N + i;
 
         float q[DK];
@@ -619,13 +622,15 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
     a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.qcode = qcode; a.scode = scode; a.recs = f->recs;
     a.qorder = f->qorder;
     a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.O = O; a.idx = idx; a.Z = Z;
-    a.N = N; a.M = p->causal ? p->chunk : N; a.total = total;
+    a.sh = make_shard(p);
+    a.nq = a.sh.slots(N);
+    a.N = N; a.M = p->causal ? p->chunk : N; a.total = BH * a.nq;
     a.k = p->k; a.W = effective_window(p); a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
     a.ws = ws;
     const int64_t per_cta = (int64_t)FWD_WARPS * FWD_QPW;
-    const unsigned grid = (unsigned)((total + per_cta - 1) / per_cta);
+    const unsigned grid = (unsigned)((a.total + per_cta - 1) / per_cta);
 #define ONEDF_FWD_R(RV) \
-    ONEDF_DISPATCH_DK(p->d_k, { topk_attn_fwd_kernel<DK, RV><<<grid, FWD_THREADS, 0, st>>>(a); })
+    ONEDF_DISPATCH_DK(p->d_k, { if (grid) topk_attn_fwd_kernel<DK, RV><<<grid, FWD_THREADS, 0, st>>>(a); })
     if (p->k <= 32) { ONEDF_FWD_R(1) }
     else if (p->k <= 64) { ONEDF_FWD_R(2) }
     else if (p->k <= 128) { ONEDF_FWD_R(4) }

@@ -27,12 +27,19 @@ int effective_bits(const onedf_problem* p);
 int effective_window(const onedf_problem* p);
 int64_t run_len_max(const onedf_problem* p);   // M (causal, capped at N) or N
 int64_t num_runs(const onedf_problem* p);
+Shard make_shard(const onedf_problem* p);      // world <= 1 -> unsharded
 
 // encode.cu
 size_t encode_ws_bytes(const onedf_problem* p, Carver* c);
 cudaError_t launch_encode(const onedf_problem* p, int b, const float* Q, const float* K, const double* lohi_in,
                           uint64_t* qcode, uint64_t* kcode, double* lohi_out, void* ws, Carver* c,
                           cudaStream_t st);
+
+// bounds-only launches (onedf_bounds_partial / _finish)
+cudaError_t launch_bounds_partial(const onedf_problem* p, const float* Q, const float* K, double* lohi, void* ws,
+                                  Carver* c, cudaStream_t st);
+cudaError_t launch_bounds_finish(const onedf_problem* p, double* lohi, void* ws, cudaStream_t st);
+cudaError_t launch_rank_sum(const float* parts, int64_t n, int32_t world, float* out, cudaStream_t st);
 
 // sort.cu
 // Global ping-pong scratch of the run sort, only for runs longer than SEG_SORT_MAX (else null).

@@ -249,13 +249,15 @@ struct TrArgs {
     uint32_t* keys_out; uint32_t* vals_out;
     uint32_t* hist; uint32_t* dtot; uint32_t* nvalid;
     int64_t L, tiles;
-    int shift, first;
+    int shift, first, k;
+    Shard sh;            // sharded: only the owned queries' slots enter the transpose
 };
 
 __device__ __forceinline__ bool tr_load(const TrArgs& a, int64_t bh, int64_t pos, uint32_t nv, uint32_t& key,
                                         uint32_t& val) {
     if (a.first) {
         if (pos >= a.L) return false;
+        if (a.sh.on() && !a.sh.owns_row(pos / a.k)) return false;
         const int32_t j = __ldg(a.idx + bh * a.L + pos);
         key = (uint32_t)j;
         val = (uint32_t)pos;
@@ -443,6 +445,7 @@ cudaError_t launch_transpose(const onedf_problem* p, const int32_t* idx, Transpo
         a.vals_out = t->vals[out];
         a.hist = t->hist; a.dtot = t->dtot; a.nvalid = t->nvalid;
         a.L = pl.L; a.tiles = pl.tiles; a.shift = 8 * ps; a.first = cur < 0;
+        a.k = p->k; a.sh = make_shard(p);
         tr_upsweep_kernel<<<grid, TR_THREADS, 0, st>>>(a);
         tr_scan_kernel<<<dim3(TR_RADIX, (unsigned)BH), 1024, 0, st>>>(a);
         tr_downsweep_kernel<<<grid, TR_THREADS, 0, st>>>(a);

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(onedf):
     for name in _declared_functions():
         assert hasattr(lib, name), name
     assert set(onedf.abi.EXPORTS) == set(_declared_functions())
-    assert onedf.onedf_version() == 200
+    assert onedf.onedf_version() == 300
 
 
 def test_struct_layout_matches_c(onedf, tmp_path):
@@ -66,6 +66,48 @@ def test_validate_rejects(onedf, field, value):
     p = onedf.Problem(*kw.values())
     assert onedf.onedf_validate(p) == onedf.abi.ERR_INVALID_ARG
     assert onedf.onedf_workspace_size(p, onedf.OP_FWD) == 0
+
+
+@pytest.mark.parametrize("rank,world,causal,want", [
+    (1, 1, 1, "ERR_INVALID_ARG"), (2, 2, 1, "ERR_INVALID_ARG"), (-1, 2, 1, "ERR_INVALID_ARG"),
+    (0, -1, 1, "ERR_INVALID_ARG"), (0, 2, 0, "ERR_UNSUPPORTED"), (1, 2, 1, "OK"), (7, 8, 1, "OK"), (0, 0, 1, "OK"),
+])
+def test_validate_shard_fields(onedf, rank, world, causal, want):
+    p = onedf.Problem(*dict(GOOD, causal=causal).values(), rank, world)
+    assert onedf.onedf_validate(p) == getattr(onedf.abi, want)
+
+
+def test_shard_owner_zigzag(onedf):
+    """Chunk c -> rank: g = c mod 2P, g < P ? g : 2P-1-g (onedf.h "Sequence sharding").  Every
+    chunk has one owner; with C a multiple of 2P every rank owns C/P chunks and the same
+    total causal work sum(c) (query i searches floor(i/M) runs)."""
+    from paper_2501_14577_b200.seqshard import ShardPlan
+    for world in (1, 2, 3, 4, 8):
+        for C in (1, 5, 32, 64):
+            own = [onedf.abi.onedf_shard_owner(c, world) for c in range(C)]
+            assert all(0 <= o < world for o in own)
+            if C % (2 * world) == 0:
+                work = [sum(c for c in range(C) if own[c] == r) for r in range(world)]
+                cnt = [own.count(r) for r in range(world)]
+                assert len(set(work)) == 1 and len(set(cnt)) == 1, (world, C, work)
+            plan = ShardPlan(N=C * 16 - 3, M=16, world=world)
+            rows = sorted(int(x) for r in range(world) for x in plan.rows[r])
+            assert rows == list(range(C * 16 - 3))          # every position owned exactly once
+            for r in range(world):
+                assert all(own[int(i) // 16] == r for i in plan.rows[r])
+    assert [onedf.abi.onedf_shard_owner(c, 4) for c in range(10)] == [0, 1, 2, 3, 3, 2, 1, 0, 0, 1]
+
+
+def test_rank_sum_checks_arguments(onedf):
+    lib = onedf.abi.lib()
+    assert lib.onedf_rank_sum(256, 10, 0, 256, None) == onedf.abi.ERR_INVALID_ARG
+    assert lib.onedf_rank_sum(None, 10, 2, 256, None) == onedf.abi.ERR_INVALID_ARG
+    sharded = onedf.Problem(*GOOD.values(), 1, 2)
+    # sharded encode needs caller bounds (the all-reduced bounds_partial); checked before the device
+    assert lib.onedf_encode(ctypes.byref(sharded), 256, 256, None, 256, 256, None, 256, 1 << 30,
+                            None) == onedf.abi.ERR_INVALID_ARG
+    assert lib.onedf_topk_attn_step_host(ctypes.byref(sharded), *([256] * 3), ctypes.c_float(0.5), *([256] * 7),
+                                         1 << 40, None) == onedf.abi.ERR_UNSUPPORTED
 
 
 def test_validate_accepts_and_sizes(onedf):
