@@ -39,7 +39,7 @@ class _Problem(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int64), ("H", ctypes.c_int64), ("N", ctypes.c_int64),
                 ("d_k", ctypes.c_int32), ("d_v", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("window", ctypes.c_int32), ("chunk", ctypes.c_int32), ("bits", ctypes.c_int32),
-                ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32)]
+                ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32), ("score", ctypes.c_int32)]
 
 
 @dataclass
@@ -55,6 +55,7 @@ class Problem:
     bits: int = 0          # 0 -> min(63 // d_k, 32) (reading D11)
     causal: int = 1
     mean_slot: int = 1
+    score: int = 0         # 0 Cauchy (Eq. 5); 1 neg-Euclidean exp, 2 inverse Euclidean, 3 dot product (D24)
 
     @property
     def BH(self) -> int:
@@ -70,11 +71,11 @@ class Problem:
 
     def c(self) -> _Problem:
         return _Problem(self.B, self.H, self.N, self.d_k, self.d_v, self.k, self.window, self.chunk,
-                        self.bits, self.causal, self.mean_slot)
+                        self.bits, self.causal, self.mean_slot, self.score)
 
     def slice(self, n_bh: int) -> "Problem":
         return Problem(1, n_bh, self.N, self.d_k, self.d_v, self.k, self.window, self.chunk, self.bits,
-                       self.causal, self.mean_slot)
+                       self.causal, self.mean_slot, self.score)
 
 
 _lib = None
@@ -100,6 +101,8 @@ def lib():
             "oref_forward": (ctypes.c_int, [P, vp, vp, vp, ctypes.c_double, vp, vp, vp, ctypes.c_int64, vp]),
             "oref_backward": (ctypes.c_int, [P, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp, vp, vp]),
             "oref_bruteforce_knn": (ctypes.c_int, [P, vp, vp, vp]),
+            "oref_forward_score": (ctypes.c_int, [P, vp, vp, vp, vp, vp, vp]),
+            "oref_backward_score": (ctypes.c_int, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "oref_num_threads": (ctypes.c_int, []),
         }
         for name, (res, args) in sig.items():
@@ -208,6 +211,13 @@ def select(p: Problem, Q, K, qcode, scode, perm, sel=None):
 
 def forward(p: Problem, Q, K, V, eps: float, idx, sel=None):
     Q = _c(Q, np.float32); K = _c(K, np.float32); V = _c(V, np.float32); idx = _c(idx, np.int32)
+    if p.score:
+        # score variants (D24): all queries; eps unused
+        assert sel is None, "score variants: all queries only"
+        O = np.zeros((p.B, p.H, p.N, p.d_v), dtype=np.float64)
+        Z = np.zeros((p.B, p.H, p.N), dtype=np.float64)
+        _check(lib().oref_forward_score(ctypes.byref(p.c()), _ptr(Q), _ptr(K), _ptr(V), _ptr(idx), _ptr(O), _ptr(Z)))
+        return O, Z
     n, s = _sel(sel)
     if s is None:
         O = np.zeros((p.B, p.H, p.N, p.d_v), dtype=np.float64)
@@ -227,6 +237,10 @@ def backward(p: Problem, Q, K, V, eps: float, idx, dO):
     dK = np.zeros((p.B, p.H, p.N, p.d_k), dtype=np.float64)
     dV = np.zeros((p.B, p.H, p.N, p.d_v), dtype=np.float64)
     d_eps = ctypes.c_double()
+    if p.score:
+        _check(lib().oref_backward_score(ctypes.byref(p.c()), _ptr(Q), _ptr(K), _ptr(V), _ptr(idx), _ptr(dO),
+                                         _ptr(dQ), _ptr(dK), _ptr(dV), ctypes.byref(d_eps)))
+        return dQ, dK, dV, d_eps.value
     _check(lib().oref_backward(ctypes.byref(p.c()), _ptr(Q), _ptr(K), _ptr(V), float(eps), _ptr(idx), _ptr(dO),
                                _ptr(dQ), _ptr(dK), _ptr(dV), ctypes.byref(d_eps)))
     return dQ, dK, dV, d_eps.value

@@ -44,6 +44,7 @@ typedef struct {
     int32_t bits;       /* b; 0 -> min(floor(63/d_k), 32) (D11) */
     int32_t causal;
     int32_t mean_slot;
+    int32_t score;      /* 0 Cauchy (Eq. 5); 1..3 the comparison operators (reading D24) */
 } oref_problem;
 
 enum { OREF_OK = 0, OREF_ERR_INVALID_ARG = 1, OREF_ERR_NONFINITE = 4 };
@@ -521,6 +522,206 @@ int oref_backward(const oref_problem* p, const float* Q, const float* K, const f
     for (int64_t bh = 0; bh < BH; ++bh) s += eps_part[bh];
     *d_eps = s;
     free(eps_part);
+    return OREF_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Score variants (reading D24).  The paper compares its
+ * Cauchy Softmax with "Negative Euclidean, ... and Inverse Euclidean
+ * operators" and with "Normalized Dot Prod" (Table
+ * "similarity metrics"); SPEC fixes their formulas:
+ *   1 NEG_EUCLID  S = exp(-D)                       ("Negative Euclidean with
+ *                                                    traditional softmax")
+ *   2 INV_EUCLID  S = 1/(sqrt(D) + 1e-6)            (stabiliser S:401)
+ *   3 DOT         S = exp(q.k / sqrt(d_k))          ("dot_product")
+ * with D = ||q - k||^2.  The top-k set is the same Euclidean selection for
+ * every score ("We utilize Euclidean distance for k-NN searches"); only
+ * the weights change: A = S/Z, Z = sum S, o = sum A v, the mean slot scored
+ * like a key.  Z output: sum S for INV_EUCLID, log(sum S) for the two
+ * exponential scores (the softmax normaliser in log form; the CUDA path keeps
+ * it in log form to stay finite).  Backward, by the chain rule with
+ * g_j = dL/dS_j = dO.(v_j - o)/Z (D15's dot product):
+ *   dq  += g_j dS_j/dq,  dk_j += g_j dS_j/dk_j,  dv_j += A_j dO
+ * where for the distance scores dS/dq = -dS/dk = S'(D) 2 (q - k) and for DOT
+ * dS/dq = S k/sqrt(d_k), dS/dk = S q/sqrt(d_k).  INV_EUCLID at D = 0 (q == k)
+ * is not differentiable; its (q - k) factor is 0 there and the gradient term is
+ * taken as 0.  No eps: d_eps = 0.                                            */
+enum { OREF_CAUCHY = 0, OREF_NEG_EUCLID = 1, OREF_INV_EUCLID = 2, OREF_DOT = 3 };
+
+/* S of one slot and its partial derivatives: gq = dS/dq, gk = dS/dk (d_k each) */
+static double score_slot(int score, const float* q, const double* kk, int dk, double* gq, double* gk) {
+    double D = 0.0, dot = 0.0;
+    for (int d = 0; d < dk; ++d) {
+        double t = (double)q[d] - kk[d];
+        D += t * t;
+        dot += (double)q[d] * kk[d];
+    }
+    double S = 0.0, dSdD = 0.0;
+    if (score == OREF_NEG_EUCLID) {
+        S = exp(-D);
+        dSdD = -S;
+    } else if (score == OREF_INV_EUCLID) {
+        double r = sqrt(D);
+        S = 1.0 / (r + 1e-6);
+        dSdD = r > 0.0 ? -S * S / (2.0 * r) : 0.0;
+    } else {  /* OREF_DOT */
+        double sc = 1.0 / sqrt((double)dk);
+        S = exp(dot * sc);
+        for (int d = 0; d < dk; ++d) { gq[d] = S * kk[d] * sc; gk[d] = S * (double)q[d] * sc; }
+        return S;
+    }
+    for (int d = 0; d < dk; ++d) {
+        double t = (double)q[d] - kk[d];
+        gq[d] = dSdD * 2.0 * t;
+        gk[d] = -dSdD * 2.0 * t;
+    }
+    return S;
+}
+
+static void key_row(const float* K, int64_t row, int dk, double* kk) {
+    for (int d = 0; d < dk; ++d) kk[d] = (double)K[row * dk + d];
+}
+
+/* forward of every query with a given index set, score variant p->score != 0 */
+int oref_forward_score(const oref_problem* p, const float* Q, const float* K, const float* V, const int32_t* idx,
+                       double* O, double* Z) {
+    const int64_t BH = p->B * p->H, N = p->N;
+    const int dk = p->d_k, dv = p->d_v, k = p->k;
+    if (p->score < 1 || p->score > 3) return OREF_ERR_INVALID_ARG;
+    #pragma omp parallel for schedule(dynamic)
+    for (int64_t bh = 0; bh < BH; ++bh) {
+        double* Kb = NULL; double* Vb = NULL;
+        double kk[8], gq[8], gk[8];
+        double* S = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+        if (p->mean_slot) {
+            Kb = (double*)malloc(sizeof(double) * (size_t)(N * dk));
+            Vb = (double*)malloc(sizeof(double) * (size_t)(N * dv));
+            prefix_means(p, K, bh, dk, Kb);
+            prefix_means(p, V, bh, dv, Vb);
+        }
+        for (int64_t i = 0; i < N; ++i) {
+            const int64_t fi = bh * N + i;
+            const float* q = Q + fi * dk;
+            const int32_t* row = idx + fi * k;
+            double Zi = 0.0;
+            int any = 0;
+            for (int r = 0; r < k; ++r) {
+                if (row[r] < 0) continue;
+                key_row(K, bh * N + row[r], dk, kk);
+                S[r] = score_slot(p->score, q, kk, dk, gq, gk);
+                Zi += S[r];
+                any = 1;
+            }
+            if (p->mean_slot) {
+                S[k] = score_slot(p->score, q, Kb + (p->causal ? i : 0) * dk, dk, gq, gk);
+                Zi += S[k];
+                any = 1;
+            }
+            for (int d = 0; d < dv; ++d) O[fi * dv + d] = 0.0;
+            if (any) {
+                for (int r = 0; r < k; ++r) {
+                    if (row[r] < 0) continue;
+                    for (int d = 0; d < dv; ++d) O[fi * dv + d] += (S[r] / Zi) * (double)V[(bh * N + row[r]) * dv + d];
+                }
+                if (p->mean_slot)
+                    for (int d = 0; d < dv; ++d) O[fi * dv + d] += (S[k] / Zi) * Vb[(p->causal ? i : 0) * dv + d];
+            }
+            Z[fi] = !any ? 0.0 : (p->score == OREF_INV_EUCLID ? Zi : log(Zi));
+        }
+        free(S); free(Kb); free(Vb);
+    }
+    return OREF_OK;
+}
+
+/* backward of every query with a given index set, score variant p->score != 0 */
+int oref_backward_score(const oref_problem* p, const float* Q, const float* K, const float* V, const int32_t* idx,
+                        const float* dO, double* dQ, double* dK, double* dV, double* d_eps) {
+    const int64_t BH = p->B * p->H, N = p->N;
+    const int dk = p->d_k, dv = p->d_v, k = p->k;
+    if (p->score < 1 || p->score > 3) return OREF_ERR_INVALID_ARG;
+    #pragma omp parallel for schedule(dynamic)
+    for (int64_t bh = 0; bh < BH; ++bh) {
+        double* Kb = NULL; double* Vb = NULL; double* dKb = NULL; double* dVb = NULL;
+        double kk[8], gq[8], gk[8];
+        double* S = (double*)malloc(sizeof(double) * (size_t)(k + 1));
+        double* o = (double*)malloc(sizeof(double) * (size_t)dv);
+        if (p->mean_slot) {
+            Kb = (double*)malloc(sizeof(double) * (size_t)(N * dk));
+            Vb = (double*)malloc(sizeof(double) * (size_t)(N * dv));
+            dKb = (double*)calloc((size_t)(N * dk), sizeof(double));
+            dVb = (double*)calloc((size_t)(N * dv), sizeof(double));
+            prefix_means(p, K, bh, dk, Kb);
+            prefix_means(p, V, bh, dv, Vb);
+        }
+        for (int64_t x = 0; x < N * dk; ++x) { dQ[bh * N * dk + x] = 0.0; dK[bh * N * dk + x] = 0.0; }
+        for (int64_t x = 0; x < N * dv; ++x) dV[bh * N * dv + x] = 0.0;
+        for (int64_t i = 0; i < N; ++i) {
+            const int64_t fi = bh * N + i;
+            const float* q = Q + fi * dk;
+            const float* g_o = dO + fi * dv;
+            const int32_t* row = idx + fi * k;
+            const int64_t mi = p->causal ? i : 0;
+            double Zi = 0.0;
+            int any = 0;
+            for (int r = 0; r < k; ++r) {
+                if (row[r] < 0) continue;
+                key_row(K, bh * N + row[r], dk, kk);
+                S[r] = score_slot(p->score, q, kk, dk, gq, gk);
+                Zi += S[r];
+                any = 1;
+            }
+            if (p->mean_slot) { S[k] = score_slot(p->score, q, Kb + mi * dk, dk, gq, gk); Zi += S[k]; any = 1; }
+            if (!any) continue;                               /* D7: nothing attended */
+            for (int d = 0; d < dv; ++d) o[d] = 0.0;
+            for (int r = 0; r < k; ++r) {
+                if (row[r] < 0) continue;
+                for (int d = 0; d < dv; ++d) o[d] += (S[r] / Zi) * (double)V[(bh * N + row[r]) * dv + d];
+            }
+            if (p->mean_slot)
+                for (int d = 0; d < dv; ++d) o[d] += (S[k] / Zi) * Vb[mi * dv + d];
+            for (int r = 0; r < k; ++r) {
+                if (row[r] < 0) continue;
+                const int64_t j = bh * N + row[r];
+                key_row(K, j, dk, kk);
+                score_slot(p->score, q, kk, dk, gq, gk);
+                double dot = 0.0;
+                for (int d = 0; d < dv; ++d) dot += (double)g_o[d] * ((double)V[j * dv + d] - o[d]);
+                const double g = dot / Zi;
+                for (int d = 0; d < dv; ++d) dV[j * dv + d] += (S[r] / Zi) * (double)g_o[d];
+                for (int d = 0; d < dk; ++d) { dQ[fi * dk + d] += g * gq[d]; dK[j * dk + d] += g * gk[d]; }
+            }
+            if (p->mean_slot) {
+                score_slot(p->score, q, Kb + mi * dk, dk, gq, gk);
+                double dot = 0.0;
+                for (int d = 0; d < dv; ++d) dot += (double)g_o[d] * (Vb[mi * dv + d] - o[d]);
+                const double g = dot / Zi;
+                for (int d = 0; d < dv; ++d) dVb[mi * dv + d] += (S[k] / Zi) * (double)g_o[d];
+                for (int d = 0; d < dk; ++d) { dQ[fi * dk + d] += g * gq[d]; dKb[mi * dk + d] += g * gk[d]; }
+            }
+        }
+        if (p->mean_slot) {
+            /* the same chain rule through the prefix means as oref_backward (S:323(a)) */
+            double* acc = (double*)calloc((size_t)(dk + dv), sizeof(double));
+            if (p->causal) {
+                for (int64_t t = N - 1; t >= 0; --t) {
+                    for (int d = 0; d < dk; ++d) acc[d] += dKb[t * dk + d] / (double)(t + 1);
+                    for (int d = 0; d < dv; ++d) acc[dk + d] += dVb[t * dv + d] / (double)(t + 1);
+                    for (int d = 0; d < dk; ++d) dK[(bh * N + t) * dk + d] += acc[d];
+                    for (int d = 0; d < dv; ++d) dV[(bh * N + t) * dv + d] += acc[dk + d];
+                }
+            } else {
+                for (int d = 0; d < dk; ++d) acc[d] = dKb[d];
+                for (int d = 0; d < dv; ++d) acc[dk + d] = dVb[d];
+                for (int64_t t = 0; t < N; ++t) {
+                    for (int d = 0; d < dk; ++d) dK[(bh * N + t) * dk + d] += acc[d] / (double)N;
+                    for (int d = 0; d < dv; ++d) dV[(bh * N + t) * dv + d] += acc[dk + d] / (double)N;
+                }
+            }
+            free(acc);
+        }
+        free(S); free(o); free(Kb); free(Vb); free(dKb); free(dVb);
+    }
+    *d_eps = 0.0;
     return OREF_OK;
 }
 

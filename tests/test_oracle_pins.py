@@ -438,3 +438,134 @@ def test_backward_invariants(causal):
     np.testing.assert_allclose(dV.sum(2), dO.astype(np.float64).sum(2), atol=1e-11)
     euler = (Q * dQ).sum() + (K * dK).sum() + 2 * eps * out["d_eps"]
     assert abs(euler) < 1e-11 * (np.abs(Q * dQ).sum() + 1)
+
+
+# --------------------------------------------------------------------------- score variants (NEXT-2, D24)
+SCORES = {1: "neg_euclid", 2: "inv_euclid", 3: "dot"}
+
+
+def _dense_causal_score(Q, K, V, score):
+    """Independent O(N^2) forms of SPEC's dense_causal_attention for the variants:
+    M = 1, k, W >= N => every j < i plus the inclusive-prefix-mean slot; weights per S:380."""
+    Q = Q.astype(np.float64); K = K.astype(np.float64); V = V.astype(np.float64)
+    N, dk = Q.shape
+    cnt = np.arange(1, N + 1)[:, None]
+    Kb = np.cumsum(K, 0) / cnt
+    Vb = np.cumsum(V, 0) / cnt
+    D = ((Q[:, None, :] - K[None, :, :]) ** 2).sum(-1)
+    Dmu = ((Q - Kb) ** 2).sum(-1)
+    if score == 1:
+        S, Smu = np.exp(-D), np.exp(-Dmu)
+    elif score == 2:
+        S, Smu = 1.0 / (np.sqrt(D) + 1e-6), 1.0 / (np.sqrt(Dmu) + 1e-6)
+    else:
+        S, Smu = np.exp(Q @ K.T / np.sqrt(dk)), np.exp((Q * Kb).sum(-1) / np.sqrt(dk))
+    S = np.where(np.tril(np.ones((N, N), bool), -1), S, 0.0)
+    Zs = S.sum(1) + Smu
+    return (S @ V + Smu[:, None] * Vb) / Zs[:, None], Zs
+
+
+@pytest.mark.parametrize("score", list(SCORES))
+def test_score_dense_special_case(score):
+    """with M = 1 and k, W >= N every score variant is dense strict-causal attention
+    plus the mean slot; Z is sum S (inverse Euclidean) or log sum S (the exponential scores)."""
+    rng = np.random.default_rng(20 + score)
+    N, dk, dv = 40, 3, 5
+    p = Problem(1, 1, N, dk, dv, N, window=N, chunk=1, causal=1, mean_slot=1, score=score)
+    Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    V = rng.normal(size=(1, 1, N, dv)).astype(np.float32)
+    out = oracle.pipeline(p, Q, K, V, 0.5)
+    O_ref, Z_ref = _dense_causal_score(Q[0, 0], K[0, 0], V[0, 0], score)
+    np.testing.assert_allclose(out["O"][0, 0], O_ref, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(out["Z"][0, 0], Z_ref if score == 2 else np.log(Z_ref), rtol=1e-12, atol=1e-13)
+
+
+def test_score_ratio_laws():
+    """Closed-form weight ratios, read back with one-hot values: exp(-D) softmax A_a/A_b =
+    exp(D_b - D_a); inverse Euclidean A_a/A_b = (sqrt D_b + 1e-6)/(sqrt D_a + 1e-6); dot
+    A_a/A_b = exp((q.k_a - q.k_b)/sqrt d_k).  Weights sum to one."""
+    rng = np.random.default_rng(21)
+    N, dk, dv, k = 40, 3, 4, 6
+    Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    for score in SCORES:
+        p = Problem(1, 1, N, dk, dv, k, window=12, chunk=4, mean_slot=0, score=score)
+        qc, kc, _ = oracle.encode(p, Q, K)
+        sc, pm = oracle.sort(p, kc)
+        idx = oracle.select(p, Q, K, qc, sc, pm)
+        i = 37
+        sel = [j for j in idx[0, 0, i] if j >= 0]
+        A = []
+        for j in sel:
+            V = np.zeros((1, 1, N, dv), np.float32)
+            V[0, 0, j, 0] = 1.0
+            O, _ = oracle.forward(p, Q, K, V, 0.5, idx)
+            A.append(O[0, 0, i, 0])
+        q = Q[0, 0, i].astype(np.float64)
+        kk = K[0, 0, sel].astype(np.float64)
+        D = ((q - kk) ** 2).sum(-1)
+        logit = {1: -D, 2: -np.log(np.sqrt(D) + 1e-6), 3: kk @ q / np.sqrt(dk)}[score]
+        assert sum(A) == pytest.approx(1.0, abs=1e-14)
+        for a in range(len(sel)):
+            for b in range(len(sel)):
+                assert A[a] / A[b] == pytest.approx(np.exp(logit[a] - logit[b]), rel=1e-11), (score, a, b)
+
+
+@pytest.mark.parametrize("score", list(SCORES))
+@pytest.mark.parametrize("causal,mean_slot", [(1, 1), (0, 1), (1, 0)])
+def test_score_backward_matches_central_differences(score, causal, mean_slot):
+    """The variants' chain rule vs central FD of L = sum dO.O with I fixed; d_eps = 0."""
+    p, Q, K, V, dO, idx = _small_problem(causal, mean_slot, seed=30 + score)
+    p = Problem(p.B, p.H, p.N, p.d_k, p.d_v, p.k, p.window, p.chunk, p.bits, p.causal, p.mean_slot, score)
+    h = 2.0 ** -14
+
+    def loss(Q_, K_, V_):
+        O, _ = oracle.forward(p, Q_, K_, V_, 0.5, idx)
+        return float(np.sum(O * dO.astype(np.float64)))
+
+    dQ, dK, dV, d_eps = oracle.backward(p, Q, K, V, 0.5, idx, dO)
+    assert d_eps == 0.0
+    for name, X, G in (("Q", Q, dQ), ("K", K, dK), ("V", V, dV)):
+        fd = np.zeros_like(G)
+        for pos in np.ndindex(X.shape):
+            Xp = X.copy(); Xp[pos] += h
+            Xm = X.copy(); Xm[pos] -= h
+            a_p = {"Q": Q, "K": K, "V": V}; a_p[name] = Xp
+            a_m = {"Q": Q, "K": K, "V": V}; a_m[name] = Xm
+            fd[pos] = (loss(a_p["Q"], a_p["K"], a_p["V"]) - loss(a_m["Q"], a_m["K"], a_m["V"])) / (2 * h)
+        scale = np.abs(G).max()
+        np.testing.assert_allclose(G, fd, rtol=1e-5, atol=1e-6 * scale, err_msg=f"{SCORES[score]} {name}")
+
+
+@pytest.mark.parametrize("score", [1, 2])
+def test_score_backward_invariants_distance_scores(score):
+    """Distance scores depend on q - k only => sum dq + sum dk = 0 (translation); every score has
+    sum A = 1 => sum dv = sum dO."""
+    rng = np.random.default_rng(40 + score)
+    N, dk, dv, k = 150, 3, 8, 8
+    p = Problem(1, 2, N, dk, dv, k, window=16, chunk=25, causal=1, mean_slot=1, score=score)
+    Q, K = (rng.normal(size=(1, 2, N, dk)).astype(np.float32) for _ in range(2))
+    V, dO = (rng.normal(size=(1, 2, N, dv)).astype(np.float32) for _ in range(2))
+    out = oracle.pipeline(p, Q, K, V, 0.5, dO)
+    np.testing.assert_allclose(out["dQ"].sum(2) + out["dK"].sum(2), 0.0, atol=1e-11)
+    np.testing.assert_allclose(out["dV"].sum(2), dO.astype(np.float64).sum(2), atol=1e-10)
+
+
+def test_score_dot_invariants():
+    """DOT: S depends on q.k only => rotating q and k together leaves O unchanged, and
+    sum_i q_i.dq_i = sum_j k_j.dk_j (both equal sum_ij s_ij dL/ds_ij); sum dv = sum dO."""
+    rng = np.random.default_rng(44)
+    N, dk, dv, k = 150, 3, 8, 8
+    p = Problem(1, 1, N, dk, dv, k, window=16, chunk=25, causal=1, mean_slot=1, score=3)
+    Q, K = (rng.normal(size=(1, 1, N, dk)).astype(np.float32) for _ in range(2))
+    V, dO = (rng.normal(size=(1, 1, N, dv)).astype(np.float32) for _ in range(2))
+    out = oracle.pipeline(p, Q, K, V, 0.5, dO)
+    lhs = (Q.astype(np.float64) * out["dQ"]).sum()
+    rhs = (K.astype(np.float64) * out["dK"]).sum()
+    assert lhs == pytest.approx(rhs, rel=1e-10)
+    np.testing.assert_allclose(out["dV"].sum(2), dO.astype(np.float64).sum(2), atol=1e-10)
+    # 90-degree rotation in the (0,1) plane (exact in f32): same dot products, same O for the same I
+    R = np.array([[0, -1, 0], [1, 0, 0], [0, 0, 1]], np.float32)
+    O2, _ = oracle.forward(p, Q @ R.T, K @ R.T, V, 0.5, out["idx"])
+    np.testing.assert_allclose(O2, out["O"], rtol=1e-13, atol=1e-14)
