@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define ONEDF_VERSION 300
+#define ONEDF_VERSION 400
 
 typedef struct CUstream_st* onedf_stream_t;   /* == cudaStream_t */
 
@@ -78,7 +78,20 @@ typedef struct {
     int32_t mean_slot;   /* 1: append the prefix-mean token (D8); 0: off      */
     int32_t shard_rank;  /* sequence sharding (NEXT-1, see "Sequence sharding" below): */
     int32_t shard_world; /*   this rank of shard_world; shard_world 0 or 1 = unsharded  */
+    int32_t score;       /* attention weight S(q, k) of a selected slot (reading D24):  */
+                         /*   ONEDF_SCORE_CAUCHY 1/(D + eps) (Eq. 5, the method)        */
+                         /*   ONEDF_SCORE_NEG_EUCLID exp(-D), ONEDF_SCORE_INV_EUCLID    */
+                         /*   1/(sqrt(D) + 1e-6), ONEDF_SCORE_DOT exp(q.k / sqrt(d_k))  */
 } onedf_problem;
+
+/* Score variants: the paper's comparison operators
+ * ("Negative Euclidean, Cauchy Softmax ..., and Inverse Euclidean";
+ * P:2092-2105 "Normalized Dot Prod"), formulas per SPEC S:380/S:401.  The
+ * index set is the same Euclidean top-k for every score; only the
+ * weights change.  Z holds sum S for CAUCHY and INV_EUCLID and log(sum S)
+ * (the log-sum-exp) for NEG_EUCLID and DOT; eps is read only by CAUCHY and
+ * d_eps is 0 for the others. */
+enum { ONEDF_SCORE_CAUCHY = 0, ONEDF_SCORE_NEG_EUCLID = 1, ONEDF_SCORE_INV_EUCLID = 2, ONEDF_SCORE_DOT = 3 };
 
 enum {
     ONEDF_OP_ENCODE = 0,
@@ -140,7 +153,11 @@ onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const f
  * dot-product reading D15, the mean-slot chain rule (S:323(a)) and one shared
  * eps (D20).  dK/dV accumulate through a stable sort of (j, slot) pairs and
  * fixed-order f64 segment sums -- no float atomics.
- *   O, Z, idx  the forward's outputs for the same inputs.
+ *   O, Z, idx  the forward's outputs for the same inputs.  Only idx is read:
+ *              the backward recomputes the normaliser Z and c_i = dO_i . o_i
+ *              in f64 from the per-slot dots dO_i . v_j (reading R3), so no
+ *              f32-rounded forward value enters g_ij = (dO_i.v_j - c_i)/Z_i;
+ *              O and Z stay in the signature for interface stability.
  *   qcode      nullable scheduling hint: the forward's query codes.  When
  *              given, queries are visited in Morton order per chunk (better
  *              L1 reuse of the gathered V rows); outputs are bitwise the same.

@@ -58,7 +58,7 @@ struct BwdArgs {
     const float* Kbar; const float* Vbar; const int32_t* qorder;
     float* dQ; float2* coeff; float2* muco; double* eps_q;
     int64_t N, total, nq;        // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
-    int k, dv, causal, mean_slot;
+    int k, dv, causal, mean_slot, score;
     Shard sh;
     void* ws;
 };
@@ -89,6 +89,29 @@ __device__ __forceinline__ void reduce_scatter(double (&v)[T]) {
     }
 }
 
+// w of one slot (dq -= w (qt q - k), dk += w (q - kt k)) and its d_eps term,
+// from the f64 weight S (exp-shifted for the softmax scores), A = S/Z and
+// diff = dO.v - c (reading D24 for the variants).
+template <int DK>
+__device__ __forceinline__ void slot_w(int sc, const float* q, const float* kj, double ed, double S, double A,
+                                       double invZ, double diff, double& w, double& de) {
+    de = 0.0;
+    if (sc == SC_CAUCHY) {
+        const double delta = dist64<DK>(q, kj) + ed;
+        const double g = diff * invZ;
+        const double inv_d2 = 1.0 / (delta * delta);
+        w = 2.0 * g * inv_d2;
+        de = -(g * inv_d2);
+    } else if (sc == SC_INV) {
+        const double r = sqrt(dist64<DK>(q, kj));
+        w = r > 0.0 ? diff * invZ * S * S / r : 0.0;   // not differentiable at q == k, where (q - k) = 0
+    } else if (sc == SC_NEG) {
+        w = 2.0 * A * diff;
+    } else {
+        w = A * diff * (1.0 / sqrt((double)DK));
+    }
+}
+
 template <int DK, int P, int CH, int R>
 __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(const BwdArgs a) {
     constexpr int G = 32 / P;                    // rows per step
@@ -96,6 +119,7 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
     constexpr int RB = T * G;                    // rows per block
     constexpr int LOGP = P == 32 ? 5 : P == 16 ? 4 : P == 8 ? 3 : P == 4 ? 2 : P == 2 ? 1 : 0;
     constexpr int LOGT = T == 16 ? 4 : T == 8 ? 3 : T == 4 ? 2 : T == 2 ? 1 : 0;
+    __shared__ double s_part[BWD_WARPS][32 * R];  // dO_i . v_j per slot (phase 1 -> phase 2)
     const int warp = threadIdx.x / 32, lane = lane_id();
     const int64_t slot = (int64_t)blockIdx.x * BWD_WARPS + warp;
     if (slot >= a.total) return;
@@ -105,65 +129,45 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
     if (!a.sh.slot_pos(slot - bh * a.nq, N, pos)) return;      // sharded: padding of a short last chunk
     const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + bh * N + pos) : pos;
     const int64_t gq = bh * N + i;
+    const int sc = a.score;
     const float e = __ldg(a.eps);
-    if (slot == 0 && lane == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
+    if (sc == SC_CAUCHY && slot == 0 && lane == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
     const double ed = (double)e;
     const int dv = a.dv, k = a.k, nch = dv / 4;
     const int grp = lane / P, l = lane % P;
-    const double Zi = (double)__ldg(a.Z + gq);
+    // something attended (D7): the mean slot or a first selected key (idx ascending, -1 padded)
+    const bool live = a.mean_slot || __ldg(a.idx + gq * k) >= 0;
     // the idx row, lane-parallel (slot e lives on lane e % 32, register e / 32)
     int jr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e2 = r * 32 + lane;
-        jr[r] = (Zi > 0.0 && e2 < k) ? __ldg(a.idx + gq * k + e2) : -1;
+        jr[r] = (live && e2 < k) ? __ldg(a.idx + gq * k + e2) : -1;
     }
     float q[DK];
 #pragma unroll
     for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
 
-    // this lane's dO chunks (ch = l + h*P, h < CH) and c_i = dO_i . o_i (fixed-order tree)
+    // this lane's dO chunks (ch = l + h*P, h < CH)
     float4 g4[CH];
-    double cpart = 0.0;
 #pragma unroll
     for (int h = 0; h < CH; ++h) {
         const int ch = l + h * P;
-        g4[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (ch < nch) {
-            g4[h] = __ldg(reinterpret_cast<const float4*>(a.dO + gq * dv) + ch);
-            if (grp == 0) {
-                const float4 o4 = __ldg(reinterpret_cast<const float4*>(a.O + gq * dv) + ch);
-                cpart = fma((double)g4[h].x, (double)o4.x, cpart);
-                cpart = fma((double)g4[h].y, (double)o4.y, cpart);
-                cpart = fma((double)g4[h].z, (double)o4.z, cpart);
-                cpart = fma((double)g4[h].w, (double)o4.w, cpart);
-            }
-        }
+        g4[h] = ch < nch ? __ldg(reinterpret_cast<const float4*>(a.dO + gq * dv) + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const double c = warp_sum(cpart);
-    const double invZ = Zi > 0.0 ? 1.0 / Zi : 0.0;
     const int64_t mrow = a.causal ? i : 0;
-    double dq[DK];
-#pragma unroll
-    for (int d = 0; d < DK; ++d) dq[d] = 0.0;
-    double deps = 0.0;
     const float* Vb = a.V + bh * N * (int64_t)dv;
-    float2* crow = a.coeff + gq * k;
     const int owner_t = l >> (LOGP - LOGT);
     const bool owner = (l & ((1 << (LOGP - LOGT)) - 1)) == 0;
+    double* sp = s_part[warp];
 
+    // ---------------- phase 1: dO_i . v_j for every slot (f64, exact f32 products)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
         for (int h0 = 0; h0 < 32; h0 += RB) {
             const int e0 = r * 32 + h0;
             if (e0 >= k) break;                                  // warp-uniform
-            // owner: its row's j and k_j, issued before the V loads
-            const int orow = h0 + owner_t * G + grp;            // lane of the owned slot
-            const int oj = __shfl_sync(FULL, jr[r], orow & 31);
-            float kj[DK];
-#pragma unroll
-            for (int d = 0; d < DK; ++d) kj[d] = (owner && oj >= 0) ? __ldg(a.K + (bh * N + oj) * DK + d) : 0.f;
             double part[T];
             float4 x[T][CH];
 #pragma unroll
@@ -189,24 +193,11 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
             }
             reduce_scatter<P, T>(part);
             const int row = e0 + owner_t * G + grp;
-            if (owner && row < k) {
-                if (oj < 0) {
-                    crow[row] = make_float2(0.f, 0.f);
-                } else {
-                    const double delta = dist64<DK>(q, kj) + ed;
-                    const double A = (1.0 / delta) * invZ;
-                    const double g = (part[0] - c) * invZ;
-                    const double inv_d2 = 1.0 / (delta * delta);
-                    const double w = 2.0 * g * inv_d2;
-                    crow[row] = make_float2((float)A, (float)w);
-#pragma unroll
-                    for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] - (double)kj[d]);
-                    deps -= g * inv_d2;
-                }
-            }
+            if (owner && row < k) sp[row] = part[0];
         }
     }
-    if (a.mean_slot && Zi > 0.0) {
+    double dot_mu = 0.0;
+    if (a.mean_slot) {
         double dpart = 0.0;
         const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)dv;
 #pragma unroll
@@ -220,19 +211,86 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
                 dpart = fma((double)g4[h].w, (double)x.w, dpart);
             }
         }
-        const double dot = warp_sum(dpart);
-        float kb[DK];
+        dot_mu = warp_sum(dpart);
+    }
+    __syncwarp();
+
+    // ---------------- phase 2: weights, normaliser and c_i = dO_i . o_i recomputed in f64
+    // from the slot dots (c = sum A_j (dO.v_j) + A_mu dO.Vbar): no f32-rounded O or Z
+    // enters g_ij = (dO.v_j - c)/Z, which matters when one weight approaches 1.
+    float kb[DK];
+    double Smu = 0.0;
+    if (a.mean_slot) {
 #pragma unroll
         for (int d = 0; d < DK; ++d) kb[d] = __ldg(a.Kbar + (bh * (a.causal ? N : 1) + mrow) * DK + d);
-        const double delta = dist64<DK>(q, kb) + ed;
-        const double A = (1.0 / delta) * invZ;
-        const double g = (dot - c) * invZ;
-        const double inv_d2 = 1.0 / (delta * delta);
-        const double w = 2.0 * g * inv_d2;
+        Smu = score_raw<DK>(sc, q, kb, ed);
+    }
+    double Sr[R], pr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        Sr[r] = 0.0;
+        pr[r] = 0.0;
+        if (jr[r] >= 0) {
+            float kj[DK];
+#pragma unroll
+            for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + jr[r]) * DK + d);
+            Sr[r] = score_raw<DK>(sc, q, kj, ed);
+            pr[r] = sp[r * 32 + lane];
+        }
+    }
+    if (score_is_exp(sc)) {
+        double m = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < R; ++r) m = jr[r] >= 0 ? fmax(m, Sr[r]) : m;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+        if (a.mean_slot) m = fmax(m, Smu);
+#pragma unroll
+        for (int r = 0; r < R; ++r) Sr[r] = jr[r] >= 0 ? exp(Sr[r] - m) : 0.0;
+        if (a.mean_slot) Smu = exp(Smu - m);
+    }
+    double zpart = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) zpart += Sr[r];
+    const double Zi = warp_sum(zpart) + Smu;
+    const double invZ = live && Zi > 0.0 ? 1.0 / Zi : 0.0;
+    double cpart = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) cpart = fma(Sr[r] * invZ, pr[r], cpart);
+    const double c = warp_sum(cpart) + (Smu * invZ) * dot_mu;
+    const double qt = sc == SC_DOT ? 0.0 : 1.0;     // dq -= w (qt q - k): distance scores vs q.k
+    double dq[DK];
+#pragma unroll
+    for (int d = 0; d < DK; ++d) dq[d] = 0.0;
+    double deps = 0.0;
+    float2* crow = a.coeff + gq * k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int e2 = r * 32 + lane;
+        if (e2 >= k) break;
+        float2 cw = make_float2(0.f, 0.f);
+        if (jr[r] >= 0) {
+            float kj[DK];
+#pragma unroll
+            for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + jr[r]) * DK + d);
+            const double A = Sr[r] * invZ;
+            double w, de;
+            slot_w<DK>(sc, q, kj, ed, Sr[r], A, invZ, pr[r] - c, w, de);
+            cw = make_float2((float)A, (float)w);
+#pragma unroll
+            for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] * qt - (double)kj[d]);
+            deps += de;
+        }
+        crow[e2] = cw;                                       // coalesced (A, w) row for the key side
+    }
+    if (a.mean_slot) {
+        const double A = Smu * invZ;
+        double w, de;
+        slot_w<DK>(sc, q, kb, ed, Smu, A, invZ, dot_mu - c, w, de);
         if (lane == 0) {
 #pragma unroll
-            for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] - (double)kb[d]);
-            deps -= g * inv_d2;
+            for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] * qt - (double)kb[d]);
+            deps += de;
             a.muco[gq] = make_float2((float)A, (float)w);
         }
     } else if (lane == 0) {
@@ -256,6 +314,7 @@ struct KeyArgs {
     float* dK; float* dV;
     int64_t N, L, total;
     int k, dv;
+    double kt;           // dk += w (q - kt k): 1 for the distance scores, 0 for DOT
 };
 
 template <int DK, int P, int CH>
@@ -336,7 +395,7 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
         // dK: the lane owning the entry, f64, fixed entry -> lane map
         if (has) {
 #pragma unroll
-            for (int d = 0; d < DK; ++d) dk[d] += (double)aw.y * ((double)qi[d] - (double)kj[d]);
+            for (int d = 0; d < DK; ++d) dk[d] += (double)aw.y * ((double)qi[d] - a.kt * (double)kj[d]);
         }
     }
 #pragma unroll
@@ -422,6 +481,7 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     a.sh = make_shard(p);
     a.nq = a.sh.slots(N);
     a.N = N; a.total = BH * a.nq; a.k = p->k; a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
+    a.score = p->score;
     a.ws = ws;
     if (a.sh.on()) {
         // rows of queries this rank does not own stay zero: they enter the A11 scan and the eps sum
@@ -461,6 +521,7 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     ka.Q = Q; ka.K = K; ka.dO = dO; ka.coeff = b->coeff; ka.slots = t->slots; ka.offsets = t->offsets;
     ka.korder = perm;
     ka.dK = dK; ka.dV = dV; ka.N = N; ka.L = N * (int64_t)p->k; ka.total = total; ka.k = p->k; ka.dv = p->d_v;
+    ka.kt = p->score == SC_DOT ? 0.0 : 1.0;
 #define ONEDF_BWDK(PV)                                                                                 \
     ONEDF_DISPATCH_DK(p->d_k, {                                                                        \
         if constexpr (PV == 32) {                                                                      \

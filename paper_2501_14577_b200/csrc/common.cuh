@@ -119,6 +119,29 @@ struct Shard {
     }
 };
 
+// Attention scores (onedf.h ONEDF_SCORE_*, reading D24).  score_raw is the
+// weight S itself for the sum-normalised scores (CAUCHY, INV_EUCLID) and the
+// logit x (S = exp(x)) for the softmax scores (NEG_EUCLID, DOT).
+enum : int { SC_CAUCHY = 0, SC_NEG = 1, SC_INV = 2, SC_DOT = 3 };
+__host__ __device__ inline bool score_is_exp(int sc) { return sc == SC_NEG || sc == SC_DOT; }
+
+template <int DK, typename KT>
+__device__ __forceinline__ double dot64(const float* q, const KT* k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < DK; ++d) acc = fma((double)q[d], (double)k[d], acc);
+    return acc;
+}
+
+template <int DK>
+__device__ __forceinline__ double score_raw(int sc, const float* q, const float* k, double eps) {
+    if (sc == SC_DOT) return dot64<DK>(q, k) * (1.0 / sqrt((double)DK));
+    const double D = dist64<DK>(q, k);
+    if (sc == SC_CAUCHY) return 1.0 / (D + eps);
+    if (sc == SC_INV) return 1.0 / (sqrt(D) + 1e-6);
+    return -D;
+}
+
 __device__ __forceinline__ void set_flag(void* ws, unsigned bit) {
     atomicOr((unsigned*)ws, bit);
 }

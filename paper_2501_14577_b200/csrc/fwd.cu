@@ -202,7 +202,7 @@ struct FwdArgs {
     const float* Kbar; const float* Vbar;
     float* O; int32_t* idx; float* Z;
     int64_t N, M, total, nq;     // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
-    int k, W, dv, causal, mean_slot;
+    int k, W, dv, causal, mean_slot, score;
     Shard sh;
     void* ws;
 };
@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
     unsigned long long* buf = s_buf[warp];
     unsigned long long* stop = s_top[warp];
     const float e = __ldg(a.eps);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
+    if (a.score == SC_CAUCHY && blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e)))
+        set_flag(a.ws, FLAG_BAD_EPS);
     const double ed = (double)e;
     const int64_t N = a.N;
     const int k = a.k;
@@ -521,9 +522,9 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
             nsel += __popc(__ballot_sync(FULL, valid));
         }
 
-        // ---------------- A7: Cauchy weights (f64)
+        // ---------------- A7: weights (f64): Cauchy Eq. 5, or a score variant (D24)
+        const int sc = a.score;
         double Sr[R];
-        double zpart = 0.0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             Sr[r] = 0.0;
@@ -531,20 +532,36 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
                 float kj[DK];
 #pragma unroll
                 for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + jr[r]) * DK + d);
-                Sr[r] = 1.0 / (dist64<DK>(q, kj) + ed);
-                zpart += Sr[r];
+                Sr[r] = score_raw<DK>(sc, q, kj, ed);
             }
         }
-        double Zi = warp_sum(zpart);
         double Smu = 0.0;
         const int64_t mrow = a.causal ? i : 0;
         if (a.mean_slot) {
             float kb[DK];
 #pragma unroll
             for (int d = 0; d < DK; ++d) kb[d] = __ldg(a.Kbar + (bh * (a.causal ? N : 1) + mrow) * DK + d);
-            Smu = 1.0 / (dist64<DK>(q, kb) + ed);
-            Zi += Smu;
+            Smu = score_raw<DK>(sc, q, kb, ed);
         }
+        double xmax = 0.0;
+        if (score_is_exp(sc)) {
+            // softmax scores: shift by the largest logit (fixed-order warp max), S = exp(x - xmax)
+            double m = -INFINITY;
+#pragma unroll
+            for (int r = 0; r < R; ++r) m = jr[r] >= 0 ? fmax(m, Sr[r]) : m;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+            if (a.mean_slot) m = fmax(m, Smu);
+            xmax = m;
+#pragma unroll
+            for (int r = 0; r < R; ++r) Sr[r] = jr[r] >= 0 ? exp(Sr[r] - xmax) : 0.0;
+            if (a.mean_slot) Smu = exp(Smu - xmax);
+        }
+        double zpart = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) zpart += Sr[r];
+        double Zi = warp_sum(zpart);
+        if (a.mean_slot) Zi += Smu;
         const double invZ = Zi > 0.0 ? 1.0 / Zi : 0.0;
 
         // ---------------- A7: value gather, float4 chunks, lane groups over slots
@@ -604,7 +621,7 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
                     make_float4((float)acc0, (float)acc1, (float)acc2, (float)acc3);
             }
         }
-        if (lane == 0) a.Z[gq] = (float)Zi;
+        if (lane == 0) a.Z[gq] = (float)(score_is_exp(sc) ? (Zi > 0.0 ? xmax + log(Zi) : 0.0) : Zi);
     }
 }
 
@@ -626,6 +643,7 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
     a.nq = a.sh.slots(N);
     a.N = N; a.M = p->causal ? p->chunk : N; a.total = BH * a.nq;
     a.k = p->k; a.W = effective_window(p); a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
+    a.score = p->score;
     a.ws = ws;
     const int64_t per_cta = (int64_t)FWD_WARPS * FWD_QPW;
     const unsigned grid = (unsigned)((a.total + per_cta - 1) / per_cta);

@@ -50,6 +50,7 @@ struct ScanSrc {
     const float* Kbar;    // MODE 1
     const float2* muco;   // MODE 1, 2
     int C, causal;
+    double kt = 1.0;      // MODE 1: w (q - kt Kbar); 0 for the DOT score (dKbar = w q)
 };
 
 template <int MODE>
@@ -60,7 +61,7 @@ __device__ __forceinline__ double scan_value(const ScanSrc& s, int64_t bh, int64
     double y;
     if (MODE == 1) {
         const float kb = __ldg(s.Kbar + (bh * (s.causal ? N : 1) + (s.causal ? i : 0)) * s.C + c);
-        y = (double)mc.y * ((double)__ldg(s.X + row * s.C + c) - (double)kb);
+        y = (double)mc.y * ((double)__ldg(s.X + row * s.C + c) - s.kt * (double)kb);
     } else {
         y = (double)mc.x * (double)__ldg(s.X + row * s.C + c);
     }
@@ -202,7 +203,7 @@ cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const 
     const float2* mc = reinterpret_cast<const float2*>(muco);
     double* partK = m->part;
     double* partV = m->part + BH * (nt + 1) * p->d_k;
-    const ScanSrc sk{Q, m->Kbar, mc, p->d_k, p->causal};
+    const ScanSrc sk{Q, m->Kbar, mc, p->d_k, p->causal, p->score == SC_DOT ? 0.0 : 1.0};
     const ScanSrc sv{dO, nullptr, mc, p->d_v, p->causal};
     const int cwk = pow2_at_least(p->d_k), cwv = pow2_at_least(p->d_v);
     scan_tile_sums_kernel<1><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(onedf):
     for name in _declared_functions():
         assert hasattr(lib, name), name
     assert set(onedf.abi.EXPORTS) == set(_declared_functions())
-    assert onedf.onedf_version() == 300
+    assert onedf.onedf_version() == 400
 
 
 def test_struct_layout_matches_c(onedf, tmp_path):
@@ -75,6 +75,13 @@ def test_validate_rejects(onedf, field, value):
 def test_validate_shard_fields(onedf, rank, world, causal, want):
     p = onedf.Problem(*dict(GOOD, causal=causal).values(), rank, world)
     assert onedf.onedf_validate(p) == getattr(onedf.abi, want)
+
+
+def test_validate_score_field(onedf):
+    for score in range(4):
+        assert onedf.onedf_validate(onedf.Problem(*GOOD.values(), 0, 1, score)) == onedf.OK
+    for score in (-1, 4):
+        assert onedf.onedf_validate(onedf.Problem(*GOOD.values(), 0, 1, score)) == onedf.abi.ERR_INVALID_ARG
 
 
 def test_shard_owner_zigzag(onedf):
