@@ -102,6 +102,7 @@ def lib():
             "oref_backward": (ctypes.c_int, [P, vp, vp, vp, ctypes.c_double, vp, vp, vp, vp, vp, vp]),
             "oref_bruteforce_knn": (ctypes.c_int, [P, vp, vp, vp]),
             "oref_forward_score": (ctypes.c_int, [P, vp, vp, vp, vp, vp, vp]),
+            "oref_code_knn": (ctypes.c_int, [P, vp, vp, ctypes.c_int, vp]),
             "oref_backward_score": (ctypes.c_int, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "oref_num_threads": (ctypes.c_int, []),
         }
@@ -250,6 +251,14 @@ def bruteforce_knn(p: Problem, Q, K):
     Q = _c(Q, np.float32); K = _c(K, np.float32)
     idx = np.zeros((p.B, p.H, p.N, p.k), dtype=np.int32)
     _check(lib().oref_bruteforce_knn(ctypes.byref(p.c()), _ptr(Q), _ptr(K), _ptr(idx)))
+    return idx
+
+
+def code_knn(p: Problem, qcode, kcode, exclude_self: bool = False):
+    """k nearest admissible keys by |kcode - qcode| (u64), ties by position (NEXT-3 locality workload)."""
+    qcode = _c(qcode, np.uint64); kcode = _c(kcode, np.uint64)
+    idx = np.zeros((p.B, p.H, p.N, p.k), dtype=np.int32)
+    _check(lib().oref_code_knn(ctypes.byref(p.c()), _ptr(qcode), _ptr(kcode), int(bool(exclude_self)), _ptr(idx)))
     return idx
 
 

@@ -750,6 +750,48 @@ int oref_bruteforce_knn(const oref_problem* p, const float* Q, const float* K, i
     return OREF_OK;
 }
 
+/* Locality workload (Fig. 4 "overlap between the top-64
+ * nearest neighbors before and after projection"
+ * "top-64 nearest-by-|code difference| after Morton encoding").  For every
+ * query i: the admissible keys (chunk-causal as in step 5, or all N),
+ * optionally without j == i, ordered by (|kcode_j - qcode_i|, j) -- u64
+ * absolute difference, ties by position (D19) -- first k, -1 padded.  Brute
+ * force: every admissible key is scored and the list is sorted.            */
+typedef struct { uint64_t d; int32_t j; } code_cand;
+static int cmp_code_cand(const void* a, const void* b) {
+    const code_cand* x = (const code_cand*)a; const code_cand* y = (const code_cand*)b;
+    if (x->d != y->d) return x->d < y->d ? -1 : 1;
+    return (x->j > y->j) - (x->j < y->j);
+}
+
+int oref_code_knn(const oref_problem* p, const uint64_t* qcode, const uint64_t* kcode, int exclude_self,
+                  int32_t* idx) {
+    const int64_t BH = p->B * p->H, N = p->N;
+    const int k = p->k;
+    #pragma omp parallel
+    {
+        code_cand* buf = (code_cand*)malloc(sizeof(code_cand) * (size_t)N);
+        #pragma omp for schedule(dynamic, 64)
+        for (int64_t flat = 0; flat < BH * N; ++flat) {
+            const int64_t bh = flat / N, i = flat % N;
+            const int64_t lim = p->causal ? (i / p->chunk) * p->chunk : N;
+            const uint64_t qc = qcode[flat];
+            int64_t n = 0;
+            for (int64_t j = 0; j < lim; ++j) {
+                if (exclude_self && j == i) continue;
+                const uint64_t kc = kcode[bh * N + j];
+                buf[n].d = kc > qc ? kc - qc : qc - kc;
+                buf[n].j = (int32_t)j;
+                ++n;
+            }
+            qsort(buf, (size_t)n, sizeof(code_cand), cmp_code_cand);
+            for (int r = 0; r < k; ++r) idx[flat * k + r] = r < n ? buf[r].j : -1;
+        }
+        free(buf);
+    }
+    return OREF_OK;
+}
+
 int oref_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

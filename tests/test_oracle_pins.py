@@ -569,3 +569,61 @@ def test_score_dot_invariants():
     R = np.array([[0, -1, 0], [1, 0, 0], [0, 0, 1]], np.float32)
     O2, _ = oracle.forward(p, Q @ R.T, K @ R.T, V, 0.5, out["idx"])
     np.testing.assert_allclose(O2, out["O"], rtol=1e-13, atol=1e-14)
+
+
+# --------------------------------------------------------------------------- locality workload (NEXT-3)
+def test_code_knn_d1_is_exact_knn():
+    """d_K = 1 with fine quantisation and no code collisions -> the code order is the
+    value order, so the nearest by |code difference| are the exact nearest (overlap 1)."""
+    rng = np.random.default_rng(50)
+    N, k = 512, 64
+    p = Problem(2, 1, N, 1, 4, k, window=N, causal=0, mean_slot=0)
+    X = rng.normal(size=(2, 1, N, 1)).astype(np.float32)
+    qc, kc, _ = oracle.encode(p, X, X)
+    assert len(np.unique(kc[0, 0])) == N
+    got = oracle.code_knn(p, qc, kc, exclude_self=True)
+    pk = Problem(2, 1, N, 1, 4, k + 1, window=N, causal=0, mean_slot=0)
+    exact = oracle.bruteforce_knn(pk, X, X)
+    for b in range(2):
+        for i in range(N):
+            want = set(exact[b, 0, i]) - {i}
+            assert len(want) == k and set(got[b, 0, i]) == want
+
+
+def test_code_knn_is_a_contiguous_block_of_the_sorted_run():
+    """With distinct codes, the k nearest codes to q are a contiguous block of the sorted order
+    that contains q's insertion neighbourhood (a consequence of sorting), and their order is
+    (|diff|, j); N = k + 1 (self excluded) returns everything else."""
+    rng = np.random.default_rng(51)
+    N, k = 300, 16
+    p = Problem(1, 1, N, 3, 4, k, causal=0, mean_slot=0)
+    X = rng.normal(size=(1, 1, N, 3)).astype(np.float32)
+    Qx = rng.normal(size=(1, 1, N, 3)).astype(np.float32)
+    qc, kc, _ = oracle.encode(p, Qx, X)
+    idx = oracle.code_knn(p, qc, kc)
+    order = np.argsort(kc[0, 0], kind="stable")
+    rank = np.empty(N, np.int64); rank[order] = np.arange(N)
+    for i in range(N):
+        r = np.sort(rank[idx[0, 0, i]])
+        assert r[-1] - r[0] == k - 1
+        d = np.array([abs(int(kc[0, 0, j]) - int(qc[0, 0, i])) for j in idx[0, 0, i]])
+        assert np.all(np.diff(d) >= 0)
+    p2 = Problem(1, 1, k + 1, 3, 4, k, causal=0, mean_slot=0)
+    X2 = X[:, :, :k + 1].copy()
+    qc2, kc2, _ = oracle.encode(p2, X2, X2)
+    got = oracle.code_knn(p2, qc2, kc2, exclude_self=True)
+    for i in range(k + 1):
+        assert set(got[0, 0, i]) == set(range(k + 1)) - {i}
+
+
+def test_code_knn_ties_and_causality():
+    """Equal codes order by position (D19); causal admissibility j < floor(i/M)*M (D6)."""
+    p = Problem(1, 1, 12, 1, 4, 3, chunk=4, causal=1, mean_slot=0)
+    kc = np.array([[[5, 5, 5, 9, 1, 5, 5, 0, 2, 2, 2, 2]]], np.uint64)
+    qc = np.full((1, 1, 12), 5, np.uint64)
+    idx = oracle.code_knn(p, qc, kc)
+    assert idx[0, 0, 2].tolist() == [-1, -1, -1]            # chunk 0: nothing admissible
+    assert idx[0, 0, 5].tolist() == [0, 1, 2]                # keys 0..3 admissible; d = 0,0,0,4
+    assert idx[0, 0, 9].tolist() == [0, 1, 2]                # keys 0..7: five at d = 0, smallest j first
+    qc[0, 0, 11] = 2
+    assert oracle.code_knn(p, qc, kc)[0, 0, 11].tolist() == [4, 7, 0]   # d = 1 (key 4), 2 (key 7), then 3 (j = 0)
