@@ -254,6 +254,25 @@ onedf_status onedf_bounds_finish(const onedf_problem* p, double* lohi, void* ws,
 onedf_status onedf_rank_sum(const float* parts, int64_t n, int32_t world, float* out,
                             onedf_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * Locality / recall workload (Fig. 4 P:1561-1581 "overlap
+ * between the top-64 nearest neighbors before and after projection"; the k
+ * ablation P:1583-1587).
+ *
+ * onedf_code_knn: for every query i, the k keys nearest in Morton code,
+ *   ordered by (|kcode_j - qcode_i| as u64, j) ascending (ties by position,
+ *   D19), -1 padded; exclude_self != 0 drops j == i.  Reads qcode and the
+ *   sorted run (scode, perm) of onedf_encode/onedf_sort.  Non-causal problems
+ *   only (causal -> UNSUPPORTED).  idx: device int32 [B,H,N,k].  No workspace.
+ * onedf_overlap: counts[r] = |{a[r][x] : a[r][x] >= 0, a[r][x] != r mod
+ *   self_period (if self_period > 0)} ∩ {b[r][y]}| for r < rows, each index
+ *   counted once; a [rows, ka], b [rows, kb] device int32, counts device
+ *   int32 [rows].  The Fig. 4 metric is counts / k. */
+onedf_status onedf_code_knn(const onedf_problem* p, const uint64_t* qcode, const uint64_t* scode,
+                            const int32_t* perm, int32_t exclude_self, int32_t* idx, onedf_stream_t stream);
+onedf_status onedf_overlap(const int32_t* a, int32_t ka, const int32_t* b, int32_t kb, int64_t rows,
+                           int64_t self_period, int32_t* counts, onedf_stream_t stream);
+
 /* Synchronises `stream`, then reads the flag word of `ws` (a workspace
  * previously passed to encode/fwd/bwd): ONEDF_OK or ONEDF_ERR_NONFINITE. */
 onedf_status onedf_check_device_status(const void* ws, onedf_stream_t stream);

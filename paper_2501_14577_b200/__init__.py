@@ -10,7 +10,8 @@ from .abi import (OK, OP_BWD, OP_ENCODE, OP_FWD, OP_SORT, OP_STEP_HOST, OnedfErr
                   onedf_topk_attn_bwd, onedf_topk_attn_fwd, onedf_topk_attn_step_host, onedf_validate,
                   onedf_version, onedf_workspace_size, status_string)
 from .api import (HostStep, Workspace, ZetaTopkAttention, bounds_finish, bounds_partial,  # noqa: F401
-                  check_device_status, default_chunk, encode, make_problem, rank_sum, sort, topk_attn_bwd,
+                  check_device_status, code_knn, default_chunk, encode, make_problem, overlap, rank_sum, sort,
+                  topk_attn_bwd,
                   topk_attn_fwd, zeta_attention)
 
 __version__ = "0.1.0"

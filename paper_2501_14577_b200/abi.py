@@ -69,6 +69,8 @@ def _load():
         "onedf_bounds_partial": (i32, [P, vp, vp, vp, vp, sz, vp]),
         "onedf_bounds_finish": (i32, [P, vp, vp, sz, vp]),
         "onedf_rank_sum": (i32, [vp, ctypes.c_int64, ctypes.c_int32, vp, vp]),
+        "onedf_code_knn": (i32, [P, vp, vp, vp, ctypes.c_int32, vp, vp]),
+        "onedf_overlap": (i32, [vp, ctypes.c_int32, vp, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, vp, vp]),
         "onedf_check_device_status": (i32, [vp, vp]),
         "onedf_status_string": (ctypes.c_char_p, [i32]),
         "onedf_version": (i32, []),
@@ -85,6 +87,7 @@ EXPORTS = ("onedf_validate", "onedf_max_run_length", "onedf_workspace_size", "on
            "onedf_topk_attn_fwd", "onedf_topk_attn_bwd", "onedf_topk_attn_fwd_traced",
            "onedf_topk_attn_bwd_traced", "onedf_topk_attn_step_host",
            "onedf_shard_owner", "onedf_bounds_partial", "onedf_bounds_finish", "onedf_rank_sum",
+           "onedf_code_knn", "onedf_overlap",
            "onedf_check_device_status", "onedf_status_string", "onedf_version")
 
 
@@ -197,6 +200,15 @@ def onedf_bounds_finish(p, lohi, ws, ws_bytes, stream=None):
 
 def onedf_rank_sum(parts, n: int, world: int, out, stream=None):
     _check(_lib.onedf_rank_sum(_p(parts), n, world, _p(out), _stream(stream)), "onedf_rank_sum")
+
+
+def onedf_code_knn(p, qcode, scode, perm, exclude_self: bool, idx, stream=None):
+    _check(_lib.onedf_code_knn(ctypes.byref(p), _p(qcode), _p(scode), _p(perm), int(bool(exclude_self)), _p(idx),
+                               _stream(stream)), "onedf_code_knn")
+
+
+def onedf_overlap(a, ka: int, b, kb: int, rows: int, self_period: int, counts, stream=None):
+    _check(_lib.onedf_overlap(_p(a), ka, _p(b), kb, rows, self_period, _p(counts), _stream(stream)), "onedf_overlap")
 
 
 def onedf_check_device_status(ws, stream=None) -> int:

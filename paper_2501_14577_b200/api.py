@@ -90,6 +90,24 @@ def rank_sum(parts):
     return out
 
 
+def code_knn(p: Problem, qcode, scode, perm, exclude_self: bool = False):
+    """NEXT-3: k nearest keys by Morton-code distance (ties by position) -> idx [B,H,N,k] int32."""
+    idx = torch.empty((p.B, p.H, p.N, p.k), dtype=torch.int32, device=qcode.device)
+    abi.onedf_code_knn(p, _dev(qcode, torch.int64), _dev(scode, torch.int64), _dev(perm, torch.int32), exclude_self,
+                       idx)
+    return idx
+
+
+def overlap(a, b, self_period: int = 0):
+    """Per row |a ∩ b| (int32 [rows]) of index lists a [..., ka], b [..., kb]; -1 and the row's own
+    position (row mod self_period, if > 0) ignored."""
+    a, b = _dev(a, torch.int32), _dev(b, torch.int32)
+    rows = a.numel() // a.shape[-1]
+    counts = torch.empty(a.shape[:-1], dtype=torch.int32, device=a.device)
+    abi.onedf_overlap(a, a.shape[-1], b, b.shape[-1], rows, self_period, counts)
+    return counts
+
+
 def sort(p: Problem, kcode, ws: Workspace | None = None):
     """A3 -> (scode, perm)."""
     kcode = _dev(kcode, torch.int64)

@@ -352,6 +352,24 @@ onedf_status onedf_rank_sum(const float* parts, int64_t n, int32_t world, float*
     return finish(launch_rank_sum(parts, n, world, out, (cudaStream_t)stream));
 }
 
+onedf_status onedf_code_knn(const onedf_problem* p, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,
+                            int32_t exclude_self, int32_t* idx, onedf_stream_t stream) {
+    onedf_status s = validate(p);
+    if (s != ONEDF_OK) return s;
+    if (p->causal) return ONEDF_ERR_UNSUPPORTED;
+    if (!qcode || !scode || !perm || !idx) return ONEDF_ERR_INVALID_ARG;
+    if ((s = check_device()) != ONEDF_OK) return s;
+    return finish(launch_code_knn(p, qcode, scode, perm, exclude_self ? 1 : 0, idx, (cudaStream_t)stream));
+}
+
+onedf_status onedf_overlap(const int32_t* a, int32_t ka, const int32_t* b, int32_t kb, int64_t rows,
+                           int64_t self_period, int32_t* counts, onedf_stream_t stream) {
+    if (!a || !b || !counts || ka < 1 || kb < 1 || rows < 0) return ONEDF_ERR_INVALID_ARG;
+    onedf_status s = check_device();
+    if (s != ONEDF_OK) return s;
+    return finish(launch_overlap(a, ka, b, kb, rows, self_period, counts, (cudaStream_t)stream));
+}
+
 onedf_status onedf_check_device_status(const void* ws, onedf_stream_t stream) {
     if (!ws) return ONEDF_ERR_INVALID_ARG;
     unsigned flags = 0;

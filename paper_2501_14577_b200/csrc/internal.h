@@ -104,4 +104,10 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
                        const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, const MeanBufs* m,
                        BwdBufs* b, TransposeBufs* t, void* ws, cudaStream_t st, const Trace& tr);
 
+// workload.cu (NEXT-3 locality workload)
+cudaError_t launch_code_knn(const onedf_problem* p, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,
+                            int exclude_self, int32_t* idx, cudaStream_t st);
+cudaError_t launch_overlap(const int32_t* a, int ka, const int32_t* b, int kb, int64_t rows, int64_t self_period,
+                           int32_t* counts, cudaStream_t st);
+
 }  // namespace onedf

@@ -51,9 +51,10 @@ __global__ void __launch_bounds__((SMEM ? SEG_MAX_WARPS : SEG_BIG_WARPS) * 32) s
         const int nmax = (int)M;
         keys0 = reinterpret_cast<uint64_t*>(smem);
         keys1 = keys0 + nmax;
+        const int npad = (nmax + 7) & ~7;       // keeps vals1 and hist 16-B aligned for odd run lengths
         vals0 = reinterpret_cast<Pos*>(keys1 + nmax);
-        vals1 = vals0 + nmax;
-        hist = reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(vals1) + ((nmax + 7) & ~7));  // [256][nw]
+        vals1 = vals0 + npad;
+        hist = reinterpret_cast<uint32_t*>(reinterpret_cast<uint16_t*>(vals1) + npad);  // [256][nw]
     } else {
         const int64_t o = bh * N + s0;
         keys0 = scr.k[0] + o;

@@ -76,6 +76,9 @@ EDGE = {
     "N1_noncausal": dict(B=1, H=1, N=1, d_k=3, d_v=8, k=4, window=8, chunk=1, causal=0, mean_slot=1),
     "chunk_gt_N": dict(B=1, H=1, N=50, d_k=3, d_v=8, k=4, window=8, chunk=64, causal=1, mean_slot=1),
     "bits_small": dict(B=1, H=1, N=256, d_k=3, d_v=8, k=8, window=16, chunk=32, bits=3, causal=1, mean_slot=1),
+    # odd run lengths (the on-chip sort's position/histogram arrays must stay aligned)
+    "odd_runs_causal": dict(B=1, H=2, N=400, d_k=3, d_v=8, k=8, window=16, chunk=65, causal=1, mean_slot=1),
+    "odd_run_noncausal": dict(B=2, H=1, N=201, d_k=3, d_v=8, k=8, window=16, chunk=1, causal=0, mean_slot=1),
     "seg_8192": dict(B=1, H=1, N=16384, d_k=3, d_v=8, k=8, window=16, chunk=8192, causal=1, mean_slot=1),
     # runs longer than the on-chip sort limit (global-scratch sort path)
     "seg_big_causal": dict(B=1, H=2, N=20000, d_k=3, d_v=8, k=8, window=16, chunk=10000, causal=1, mean_slot=1),
