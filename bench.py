@@ -458,6 +458,7 @@ def main():
     ap.add_argument("--impl", default="onedf", choices=["onedf", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--bh", type=int, default=0, help="override B x H with 1 x BH slices (config sweeps of long N)")
     args = ap.parse_args()
     world, rank, local = _dist_env()
     if args.gpus is not None and args.gpus != world and world == 1 and args.gpus > 1:
@@ -465,6 +466,8 @@ def main():
         return 1
     import synth
     cfg = synth.CONFIGS[args.config]
+    if args.bh:
+        cfg = cfg.with_(B=1, H=args.bh)
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
         return 0
