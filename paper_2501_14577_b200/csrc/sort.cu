@@ -209,9 +209,18 @@ cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, in
 // counts, then a (digit, warp)-ordered tile scan), stages the tile digit-
 // sorted in shared memory, and writes each digit's run to its global slot
 // with consecutive threads on consecutive addresses (coalesced).
-constexpr int TR_THREADS = 256;
+#ifndef ONEDF_TR_THREADS
+#define ONEDF_TR_THREADS 256
+#endif
+#ifndef ONEDF_TR_IPT
+#define ONEDF_TR_IPT 8
+#endif
+#ifndef ONEDF_TR_MINB
+#define ONEDF_TR_MINB 4
+#endif
+constexpr int TR_THREADS = ONEDF_TR_THREADS;
 constexpr int TR_WARPS = TR_THREADS / 32;
-constexpr int TR_IPT = 8;
+constexpr int TR_IPT = ONEDF_TR_IPT;
 constexpr int TR_TILE = TR_THREADS * TR_IPT;       // 2048 pairs per tile
 constexpr int TR_RADIX = 256;
 
@@ -346,7 +355,7 @@ __global__ void __launch_bounds__(1024) tr_scan_kernel(const TrArgs a) {
     for (int64_t t = t0; t < t1; ++t) { const uint32_t x = h[t]; h[t] = run; run += x; }
 }
 
-__global__ void __launch_bounds__(TR_THREADS, 4) tr_downsweep_kernel(const TrArgs a) {
+__global__ void __launch_bounds__(TR_THREADS, ONEDF_TR_MINB) tr_downsweep_kernel(const TrArgs a) {
     __shared__ uint32_t sk[TR_TILE], sv[TR_TILE];
     __shared__ uint32_t cnt[TR_WARPS * TR_RADIX];    // [warp][digit]: a warp's random digits hit distinct banks
     __shared__ uint32_t tstart[TR_RADIX], gbase[TR_RADIX];
