@@ -270,8 +270,8 @@ def run_gpu(args, cfg, world, rank, local):
     ws = wsbuf.data_ptr() + ((-wsbuf.data_ptr()) % 256)
     stream = torch.cuda.current_stream(dev)
 
-    # stage events: 0 start | 1 encode | 2 sort | fwd: 3 means 4 records 5 topk | bwd: 6 means 7 query
-    # 8 transpose 9 key 10 scan 11 eps | 12 d_eps exchange
+    # stage events: 0 start | 1 encode | 2 sort | fwd: 3 means 4 records 5 topk | bwd: 6 means 7 CSR
+    # (transpose) 8 query 9 key 10 scan 11 eps | 12 d_eps exchange
     NEV = 13
 
     def new_events():
@@ -294,8 +294,8 @@ def run_gpu(args, cfg, world, rank, local):
             odist.combine_d_eps(d_eps)      # one f64 per rank, rank-ordered sum (D20)
         ev[12].record(stream)
 
-    stage_names = ["encode", "sort", "fwd_means", "fwd_records", "fwd_topk", "bwd_means", "bwd_query",
-                   "bwd_transpose", "bwd_key", "bwd_scans", "bwd_eps", "deps_exchange"]
+    stage_names = ["encode", "sort", "fwd_means", "fwd_records", "fwd_topk", "bwd_means", "bwd_transpose",
+                   "bwd_query", "bwd_key", "bwd_scans", "bwd_eps", "deps_exchange"]
 
     # warm-up
     for _ in range(args.warmup):
@@ -426,15 +426,13 @@ def run_gpu(args, cfg, world, rank, local):
 
 
 def count_launches(p) -> int:
-    """Kernel launches of one step (encode 2, sort 1, fwd 3 means + records + topk, bwd 3 means + query +
-    3 per radix pass + offsets + key + 3 scan + eps), derived from the same plan the library uses."""
-    n_bits = 1
-    while (1 << n_bits) <= p.N:
-        n_bits += 1
-    passes = (n_bits + 8) // 9
-    means = 3 if p.causal else 2
-    fwd = (means if p.mean_slot else 0) + 2
-    bwd = (means if p.mean_slot else 0) + 1 + 3 * passes + 1 + 1 + (3 if p.mean_slot else 0) + 1
+    """Kernel launches of one step, from the library's launch plan (checked against the ncu launch
+    list in profiles/): encode 2 (bounds partials, encode), sort 1; fwd: prefix means 6 (mean slot),
+    key records 1, Morton query schedule 1, top-k 1; bwd: prefix means 6, CSR count + scan 2, query
+    schedule 1, query side 1, key side 1, mean-slot scans 6, eps 2."""
+    means = 6 if p.mean_slot else 0
+    fwd = means + 3
+    bwd = means + 2 + 1 + 1 + 1 + means + 2
     return 2 + 1 + fwd + bwd
 
 

@@ -151,8 +151,9 @@ onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const f
 
 /* A8-A12: backward with I held fixed (D16), appendix P:2006-2045 with the
  * dot-product reading D15, the mean-slot chain rule (S:323(a)) and one shared
- * eps (D20).  dK/dV accumulate through a stable sort of (j, slot) pairs and
- * fixed-order f64 segment sums -- no float atomics.
+ * eps (D20).  dK/dV accumulate through a key-major CSR of the selected
+ * (query, slot) records (integer in-degree counts and cursors) and f64 segment
+ * sums in ascending query order -- no float atomics, bitwise reproducible.
  *   O, Z, idx  the forward's outputs for the same inputs.  Only idx is read:
  *              the backward recomputes the normaliser Z and c_i = dO_i . o_i
  *              in f64 from the per-slot dots dO_i . v_j (reading R3), so no
@@ -177,7 +178,7 @@ onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const f
  * (entries at s >= n_events, or NULL entries, are skipped).  `events` holds
  * caller-created cudaEvent_t handles.  Stages:
  *   fwd: 0 prefix means (A4)  1 sorted key records (K4)  2 top-k attention (A5-A7)
- *   bwd: 0 prefix means (A4)  1 query side (A8)  2 transpose (A9)
+ *   bwd: 0 prefix means (A4)  1 transpose: in-degree CSR (A9)  2 query side (A8)
  *        3 key side (A10)     4 mean-slot scan (A11)      5 eps reduce (A12)    */
 onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K,
                                         const float* V, const float* eps, const uint64_t* qcode,

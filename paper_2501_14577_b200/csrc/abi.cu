@@ -69,7 +69,7 @@ static onedf_status validate(const onedf_problem* p) {
 
 // ---------------------------------------------------------------- workspace layouts
 struct FwdLayout { MeanBufs m; FwdBufs f; size_t bytes; };
-struct BwdLayout { MeanBufs m; BwdBufs b; TransposeBufs t; size_t bytes; };
+struct BwdLayout { MeanBufs m; BwdBufs b; CsrBufs t; size_t bytes; };
 
 static FwdLayout fwd_layout(const onedf_problem* p, void* ws) {
     FwdLayout L;
@@ -84,7 +84,7 @@ static BwdLayout bwd_layout(const onedf_problem* p, void* ws) {
     Carver c(ws);
     mean_carve(p, &c, &L.m);
     bwd_carve(p, &c, &L.b);
-    transpose_carve(p, &c, &L.t);
+    csr_carve(p, &c, &L.t);
     L.bytes = c.bytes();
     return L;
 }

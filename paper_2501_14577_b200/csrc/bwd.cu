@@ -44,7 +44,6 @@ constexpr int MAX_DV = 256;
 
 void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b) {
     const int64_t BH = p->B * p->H, total = BH * p->N;
-    b->coeff = c->take<float2>((size_t)(total * p->k));
     b->muco = c->take<float2>((size_t)total);
     b->eps_q = c->take<double>((size_t)total);
     b->eps_part = c->take<double>((size_t)EPS_PARTS);
@@ -56,8 +55,9 @@ struct BwdArgs {
     const float* Q; const float* K; const float* V; const float* eps;
     const float* O; const float* dO; const int32_t* idx; const float* Z;
     const float* Kbar; const float* Vbar; const int32_t* qorder;
-    float* dQ; float2* coeff; float2* muco; double* eps_q;
-    int64_t N, total, nq;        // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
+    float* dQ; float2* muco; double* eps_q;
+    int32_t* cursor; int4* rec;                           // key-major CSR records (csr.cu)
+    int64_t N, total, nq, L;        // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
     int k, dv, causal, mean_slot, score;
     Shard sh;
     void* ws;
@@ -263,12 +263,12 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
 #pragma unroll
     for (int d = 0; d < DK; ++d) dq[d] = 0.0;
     double deps = 0.0;
-    float2* crow = a.coeff + gq * k;
+    int32_t* cur = a.cursor + bh * N;
+    int4* rec = a.rec + bh * a.L;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e2 = r * 32 + lane;
         if (e2 >= k) break;
-        float2 cw = make_float2(0.f, 0.f);
         if (jr[r] >= 0) {
             float kj[DK];
 #pragma unroll
@@ -276,12 +276,13 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
             const double A = Sr[r] * invZ;
             double w, de;
             slot_w<DK>(sc, q, kj, ed, Sr[r], A, invZ, pr[r] - c, w, de);
-            cw = make_float2((float)A, (float)w);
 #pragma unroll
             for (int d = 0; d < DK; ++d) dq[d] -= w * ((double)q[d] * qt - (double)kj[d]);
             deps += de;
+            // append the record to key j's CSR segment (integer slot; the key side orders by i)
+            const int32_t pos = atomicAdd(cur + jr[r], 1);
+            rec[pos] = make_int4((int32_t)i, __float_as_int((float)A), __float_as_int((float)w), 0);
         }
-        crow[e2] = cw;                                       // coalesced (A, w) row for the key side
     }
     if (a.mean_slot) {
         const double A = Smu * invZ;
@@ -309,18 +310,33 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
 }
 
 struct KeyArgs {
-    const float* Q; const float* K; const float* dO; const float2* coeff;
-    const uint32_t* slots; const int32_t* offsets; const int32_t* korder;
+    const float* Q; const float* K; const float* dO;
+    const int32_t* offsets; const int4* rec; int32_t* order;
+    const int32_t* korder;
     float* dK; float* dV;
     int64_t N, L, total;
     int k, dv;
     double kt;           // dk += w (q - kt k): 1 for the distance scores, 0 for DOT
 };
 
+constexpr int KEY_REG_SEG = 256;      // segments up to this length are ordered in registers
+constexpr int KEY_POS_BITS = 8;       // u32 sort key (i << 8 | position): needs N < 2^24
+
+template <int R>
+__device__ __forceinline__ void sort_prefix(uint32_t (&x)[8]) {
+    uint32_t y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) y[r] = x[r];
+    warp_sort_u32<R>(y);
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = y[r];
+}
+
 template <int DK, int P, int CH>
 __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(const KeyArgs a) {
     constexpr int G = 32 / P;
     constexpr int U = ONEDF_KEY_U;                // entries per lane group in flight
+    __shared__ uint32_t s_key[BWD_WARPS][KEY_REG_SEG];
     const int warp = threadIdx.x / 32, lane = lane_id();
     const int64_t slot = (int64_t)blockIdx.x * BWD_WARPS + warp;
     if (slot >= a.total) return;
@@ -329,10 +345,40 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
     const int64_t gk = bh * N + j;
     const int32_t* off = a.offsets + bh * (N + 1);
     const int32_t s0 = __ldg(off + j), s1 = __ldg(off + j + 1);
-    const uint32_t* sl = a.slots + bh * a.L;
-    const float2* cf = a.coeff + bh * a.L;
-    const int dv = a.dv, k = a.k, nch = dv / 4;
+    const int32_t len = s1 - s0;
+    const int4* rec = a.rec + bh * a.L + s0;
+    const int dv = a.dv, nch = dv / 4;
     const int grp = lane / P, l = lane % P;
+
+    // ---- fixed visiting order: ascending query position i (distinct within a segment)
+    const bool small = len <= KEY_REG_SEG && N < (1ll << (32 - KEY_POS_BITS));
+    uint32_t* sk = s_key[warp];                   // sorted (i << 8 | position) keys
+    int32_t* go = a.order + bh * a.L + s0;
+    if (small) {
+        uint32_t xs[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int e = r * 32 + lane;
+            xs[r] = e < len ? ((uint32_t)__ldg(&rec[e].x) << KEY_POS_BITS) | (uint32_t)e : ~0u;
+        }
+        if (len <= 32) sort_prefix<1>(xs);
+        else if (len <= 64) sort_prefix<2>(xs);
+        else if (len <= 128) sort_prefix<4>(xs);
+        else sort_prefix<8>(xs);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (r * 32 < len) sk[r * 32 + lane] = xs[r];
+        __syncwarp();
+    } else {
+        for (int e = lane; e < len; e += 32) {
+            const int32_t mine = __ldg(&rec[e].x);
+            int rank = 0;
+            for (int x = 0; x < len; ++x) rank += __ldg(&rec[x].x) < mine;
+            go[rank] = e;
+        }
+        __syncwarp();
+    }
+
     float kj[DK];
 #pragma unroll
     for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + gk * DK + d);
@@ -347,22 +393,28 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
     const float* dOb = a.dO + bh * N * (int64_t)dv;
     const float* Qb = a.Q + bh * N * DK;
 
-    // entry loads of the next 32-entry chunk are issued one chunk ahead
-    uint32_t sv_next = (s0 + lane < s1) ? __ldg(sl + s0 + lane) : 0u;
-    for (int32_t b0 = s0; b0 < s1; b0 += 32) {
-        const int32_t s = b0 + lane;
-        const bool has = s < s1;
-        const uint32_t sv = sv_next;
-        sv_next = (s + 32 < s1) ? __ldg(sl + s + 32) : 0u;
-        const int iq = (int)(sv / (uint32_t)k);
+    for (int32_t b0 = 0; b0 < len; b0 += 32) {
+        const int32_t t = b0 + lane;
+        const bool has = t < len;
+        int iq = 0;
         float2 aw = make_float2(0.f, 0.f);
         float qi[DK];
         if (has) {
-            aw = __ldg(cf + sv);
+            int e;
+            if (small) {
+                const uint32_t v = sk[t];
+                e = (int)(v & ((1u << KEY_POS_BITS) - 1));
+                iq = (int)(v >> KEY_POS_BITS);
+            } else {
+                e = go[t];
+                iq = __ldg(&rec[e].x);
+            }
+            const int4 rv = __ldg(rec + e);
+            aw = make_float2(__int_as_float(rv.y), __int_as_float(rv.z));
 #pragma unroll
             for (int d = 0; d < DK; ++d) qi[d] = __ldg(Qb + (int64_t)iq * DK + d);
         }
-        const int n = min(32, s1 - b0);
+        const int n = min(32, len - b0);
         // dV: group g takes entries g, g+G, ... of this chunk, U at a time
         for (int t0 = 0; t0 < n; t0 += G * U) {
             float4 x[U][CH];
@@ -465,7 +517,7 @@ static int lanes_per_row(int dv) {
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                        const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
                        const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, const MeanBufs* m,
-                       BwdBufs* b, TransposeBufs* t, void* ws, cudaStream_t st, const Trace& tr) {
+                       BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
     cudaError_t e = cudaSuccess;
     const int32_t* qorder = nullptr;
@@ -474,10 +526,15 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
         if (e != cudaSuccess) return e;
         qorder = b->qorder;
     }
+    // A9 first: in-degree counts -> CSR offsets + insertion cursors (the query side appends into them)
+    e = launch_csr_count(p, idx, qorder, t, st);
+    if (e != cudaSuccess) return e;
+    tr.mark(1, st);
     BwdArgs a;
     a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.O = O; a.dO = dO; a.idx = idx; a.Z = Z;
     a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.qorder = qorder;
-    a.dQ = dQ; a.coeff = b->coeff; a.muco = b->muco; a.eps_q = b->eps_q;
+    a.dQ = dQ; a.muco = b->muco; a.eps_q = b->eps_q;
+    a.cursor = t->cursor; a.rec = t->rec; a.L = N * (int64_t)p->k;
     a.sh = make_shard(p);
     a.nq = a.sh.slots(N);
     a.N = N; a.total = BH * a.nq; a.k = p->k; a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
@@ -513,12 +570,10 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     else { ONEDF_BWDQ(32) }
 #undef ONEDF_BWDQ
 #undef ONEDF_BWDQR
-    tr.mark(1, st);
-    e = launch_transpose(p, idx, t, st);
-    if (e != cudaSuccess) return e;
     tr.mark(2, st);
     KeyArgs ka;
-    ka.Q = Q; ka.K = K; ka.dO = dO; ka.coeff = b->coeff; ka.slots = t->slots; ka.offsets = t->offsets;
+    ka.Q = Q; ka.K = K; ka.dO = dO; ka.offsets = t->offsets; ka.rec = t->rec;
+    ka.order = t->order;
     ka.korder = perm;
     ka.dK = dK; ka.dV = dV; ka.N = N; ka.L = N * (int64_t)p->k; ka.total = total; ka.k = p->k; ka.dv = p->d_v;
     ka.kt = p->score == SC_DOT ? 0.0 : 1.0;

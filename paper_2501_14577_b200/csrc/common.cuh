@@ -85,6 +85,92 @@ __device__ __forceinline__ double dist64(const float* q, const float* k) {
     return acc;
 }
 
+// ---------------------------------------------------------------- warp sorting of u64 keys
+__device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a < b ? b : a; }
+
+// Ascending bitonic sort of one key per lane (element e = lane).
+__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long x) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const unsigned long long y = __shfl_xor_sync(FULL, x, stride);
+            const bool up = (lane & size) == 0 || size == 32;
+            const bool lower = (lane & stride) == 0;
+            x = (lower == up) ? umin64(x, y) : umax64(x, y);
+        }
+    }
+    return x;
+}
+
+// Ascending bitonic sort of 32*R keys spread over the warp (element e = r*32 + lane).
+template <int R>
+__device__ __forceinline__ void warp_sort(unsigned long long (&x)[R]) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+                const int rs = stride / 32;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if ((r & rs) == 0) {
+                        const bool up = ((r * 32) & size) == 0;
+                        const unsigned long long a = x[r], b = x[r + rs];
+                        const unsigned long long lo = umin64(a, b), hi = umax64(a, b);
+                        x[r] = up ? lo : hi;
+                        x[r + rs] = up ? hi : lo;
+                    }
+                }
+            } else {
+                const bool lower = (lane & stride) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const bool up = size >= 32 ? ((r * 32) & size) == 0 : (lane & size) == 0;
+                    const unsigned long long y = __shfl_xor_sync(FULL, x[r], stride);
+                    x[r] = (lower == up) ? umin64(x[r], y) : umax64(x[r], y);
+                }
+            }
+        }
+    }
+}
+
+// Ascending bitonic sort of 32*R u32 keys spread over the warp (element e = r*32 + lane).
+template <int R>
+__device__ __forceinline__ void warp_sort_u32(uint32_t (&x)[R]) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= 32) {
+                const int rs = stride / 32;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if ((r & rs) == 0) {
+                        const bool up = ((r * 32) & size) == 0;
+                        const uint32_t a = x[r], b = x[r + rs];
+                        const uint32_t lo = min(a, b), hi = max(a, b);
+                        x[r] = up ? lo : hi;
+                        x[r + rs] = up ? hi : lo;
+                    }
+                }
+            } else {
+                const bool lower = (lane & stride) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const bool up = size >= 32 ? ((r * 32) & size) == 0 : (lane & size) == 0;
+                    const uint32_t y = __shfl_xor_sync(FULL, x[r], stride);
+                    x[r] = (lower == up) ? min(x[r], y) : max(x[r], y);
+                }
+            }
+        }
+    }
+}
+
 // Sequence sharding (onedf.h "Sequence sharding"): chunk c of every (b,h)
 // belongs to rank owner(c) (zig-zag over 2*world); a rank computes the
 // queries of its chunks.  world <= 1: everything is owned.

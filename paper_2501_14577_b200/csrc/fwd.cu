@@ -87,25 +87,6 @@ __global__ void build_records_kernel(const float* __restrict__ K, const int32_t*
 }
 
 // ------------------------------------------------------------------ register top-k
-__device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) { return a < b ? a : b; }
-__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) { return a < b ? b : a; }
-
-// Ascending bitonic sort of one key per lane (element e = lane).
-__device__ __forceinline__ unsigned long long warp_sort32(unsigned long long x) {
-    const int lane = lane_id();
-#pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const unsigned long long y = __shfl_xor_sync(FULL, x, stride);
-            const bool up = (lane & size) == 0 || size == 32;
-            const bool lower = (lane & stride) == 0;
-            x = (lower == up) ? umin64(x, y) : umax64(x, y);
-        }
-    }
-    return x;
-}
-
 // Merge the 32 pending keys (one per lane, unsorted; KEY_MAX = empty) into the
 // ascending top list top[R] (element e = r*32 + lane), keeping the lowest 32R.
 template <int R>
@@ -145,39 +126,6 @@ __device__ __forceinline__ unsigned long long list_get(const unsigned long long 
 #pragma unroll
     for (int r = 1; r < R; ++r) v = (e >> 5) == r ? top[r] : v;
     return __shfl_sync(FULL, v, e & 31);
-}
-
-// Ascending bitonic sort of 32*R keys spread over the warp (element e = r*32 + lane).
-template <int R>
-__device__ __forceinline__ void warp_sort(unsigned long long (&x)[R]) {
-    const int lane = lane_id();
-#pragma unroll
-    for (int size = 2; size <= 32 * R; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            if (stride >= 32) {
-                const int rs = stride / 32;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    if ((r & rs) == 0) {
-                        const bool up = ((r * 32) & size) == 0;
-                        const unsigned long long a = x[r], b = x[r + rs];
-                        const unsigned long long lo = umin64(a, b), hi = umax64(a, b);
-                        x[r] = up ? lo : hi;
-                        x[r + rs] = up ? hi : lo;
-                    }
-                }
-            } else {
-                const bool lower = (lane & stride) == 0;
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    const bool up = size >= 32 ? ((r * 32) & size) == 0 : (lane & size) == 0;
-                    const unsigned long long y = __shfl_xor_sync(FULL, x[r], stride);
-                    x[r] = (lower == up) ? umin64(x[r], y) : umax64(x[r], y);
-                }
-            }
-        }
-    }
 }
 
 // The first 32*RO keys (ascending) of buf[0..cnt) (unique keys), sorted as 32*RS.

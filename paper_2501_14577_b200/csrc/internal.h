@@ -52,17 +52,19 @@ cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint6
                             int32_t* perm, const SortScratch& scr, cudaStream_t st);
 cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, int32_t* qorder,
                                const SortScratch& scr, cudaStream_t st);
-struct TransposeBufs {
-    uint32_t* keys[2];
-    uint32_t* vals[2];
-    uint32_t* hist;     // [BH][256][tiles] per-tile digit counts -> tile offsets within the digit
-    uint32_t* dtot;     // [BH][256] digit totals of the current pass
-    uint32_t* nvalid;   // [BH] valid (j >= 0) pairs
-    int32_t* offsets;   // [BH][N+1]  CSR: slots of key j are sorted[off[j], off[j+1])
-    uint32_t* slots;    // final sorted slot ids (points into vals)
+
+
+// csr.cu -- A9 key-major CSR of the selected (query, slot) records
+struct CsrBufs {
+    int32_t* cursor;    // [BH][N]    in-degree counts -> insertion cursors
+    int32_t* offsets;   // [BH][N+1]  segment of key j = records [off[j], off[j+1])
+    int4* rec;          // [BH][N*k]  record {i, A bits, w bits, 0} of each selected (query, slot)
+    int32_t* order;     // [BH][N*k]  ascending-i order of segments longer than the on-chip limit
 };
-void transpose_carve(const onedf_problem* p, Carver* c, TransposeBufs* t);
-cudaError_t launch_transpose(const onedf_problem* p, const int32_t* idx, TransposeBufs* t, cudaStream_t st);
+void csr_carve(const onedf_problem* p, Carver* c, CsrBufs* t);
+// qorder: the query schedule (nullable -> natural order); only its grouping of similar queries matters
+cudaError_t launch_csr_count(const onedf_problem* p, const int32_t* idx, const int32_t* qorder, CsrBufs* t,
+                             cudaStream_t st);
 
 // mean.cu
 struct MeanBufs {
@@ -91,7 +93,6 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
 // bwd.cu
 constexpr int EPS_PARTS = 1024;   // fixed first-level split of the d_eps reduction
 struct BwdBufs {
-    float2* coeff;      // [BH][N][k] (A, w)
     float2* muco;       // [BH][N]    (A_mu, w_mu)
     double* eps_q;      // [BH][N]    per-query d_eps contribution
     double* eps_part;   // [EPS_PARTS]
@@ -102,7 +103,7 @@ void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b);
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                        const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
                        const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, const MeanBufs* m,
-                       BwdBufs* b, TransposeBufs* t, void* ws, cudaStream_t st, const Trace& tr);
+                       BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr);
 
 // workload.cu (NEXT-3 locality workload)
 cudaError_t launch_code_knn(const onedf_problem* p, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,
