@@ -236,6 +236,32 @@ def test_determinism_bitwise():
         assert np.array_equal(np.atleast_1d(a[n]).view(np.uint8), np.atleast_1d(b[n]).view(np.uint8)), n
 
 
+def _hub_inputs(kw, seed, vocab=4):
+    """Few distinct key rows: the lowest-position copies of each token are selected by most
+    queries, so key in-degrees exceed the key side's on-chip segment limit (256)."""
+    rng = np.random.default_rng(seed)
+    B, H, N, dk, dv = kw["B"], kw["H"], kw["N"], kw["d_k"], kw["d_v"]
+    voc = rng.normal(size=(vocab, dk)).astype(np.float32)
+    tok = rng.integers(0, vocab, size=(B, H, N))
+    return dict(K=voc[tok], Q=(voc[tok] + 0.01 * rng.normal(size=(B, H, N, dk))).astype(np.float32),
+                V=rng.normal(size=(B, H, N, dv)).astype(np.float32),
+                dO=rng.normal(size=(B, H, N, dv)).astype(np.float32))
+
+
+@pytest.mark.parametrize("causal", [1, 0])
+def test_hub_keys_long_segments_parity_and_determinism(causal):
+    kw = dict(B=1, H=2, N=2048, d_k=3, d_v=16, k=32, window=64, chunk=256, causal=causal, mean_slot=1)
+    x = _hub_inputs(kw, seed=5 + causal)
+    a = gpu_run(kw, x)
+    ref = oracle_run(kw, x)
+    indeg = np.bincount(a["idx"][a["idx"] >= 0].ravel(), minlength=1)
+    assert indeg.max() > 256                       # the long-segment path is exercised
+    _compare_all(a, ref)
+    b = gpu_run(kw, x)
+    for n in ("dQ", "dK", "dV", "d_eps"):
+        assert np.array_equal(np.atleast_1d(a[n]).view(np.uint8), np.atleast_1d(b[n]).view(np.uint8)), n
+
+
 def test_nonfinite_and_bad_eps_flags():
     import torch
 
