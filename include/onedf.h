@@ -197,6 +197,12 @@ onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, 
  * metric times): async H2D copies of Q, K, V, dO (host pointers; pinned for
  * full speed), then encode -> sort -> fwd -> bwd on the device, then async
  * D2H copies of O, dQ, dK, dV (host pointers) and d_eps (host double*).
+ * The (b,h) slices are processed in up to 8 groups: the H2D copy of the next
+ * group and the D2H copy of the previous one run on two internal streams
+ * (created and released by the call, ordered by events) while `stream`
+ * computes the current group, so PCIe traffic overlaps the kernels.  Every
+ * slice's outputs equal the device path's bit for bit; d_eps is the groups'
+ * partial sums added in group order.
  * eps is passed by value.  All device buffers live in `ws` (device,
  * onedf_workspace_size(p, ONEDF_OP_STEP_HOST) bytes).  Returns after
  * enqueueing; synchronise `stream` before reading the host outputs. */

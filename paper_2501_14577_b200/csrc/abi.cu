@@ -99,6 +99,10 @@ static size_t sort_bytes(const onedf_problem* p) {
     return c.bytes();
 }
 
+// The host-buffer step pipelines groups of (b,h) slices: H2D of group g+1 and
+// D2H of group g-1 overlap the compute of group g (three streams, events).
+constexpr int STEP_GROUPS_MAX = 8;
+
 struct StepLayout {
     float *Q, *K, *V, *dO, *O, *dQ, *dK, *dV, *Z, *eps;
     double* d_eps;
@@ -117,7 +121,7 @@ static StepLayout step_layout(const onedf_problem* p, void* ws) {
     const int64_t BH = p->B * p->H, N = p->N, nk = BH * N * p->d_k, nv = BH * N * p->d_v;
     L.Q = c.take<float>(nk); L.K = c.take<float>(nk); L.V = c.take<float>(nv); L.dO = c.take<float>(nv);
     L.O = c.take<float>(nv); L.dQ = c.take<float>(nk); L.dK = c.take<float>(nk); L.dV = c.take<float>(nv);
-    L.Z = c.take<float>(BH * N); L.eps = c.take<float>(1); L.d_eps = c.take<double>(1);
+    L.Z = c.take<float>(BH * N); L.eps = c.take<float>(1); L.d_eps = c.take<double>(STEP_GROUPS_MAX + 1);
     L.qcode = c.take<uint64_t>(BH * N); L.kcode = c.take<uint64_t>(BH * N); L.scode = c.take<uint64_t>(BH * N);
     L.perm = c.take<int32_t>(BH * N); L.idx = c.take<int32_t>(BH * N * p->k);
     c.take<char>(0);
@@ -129,6 +133,13 @@ static StepLayout step_layout(const onedf_problem* p, void* ws) {
 }
 
 __global__ void set_scalar_kernel(float* dst, float v) { *dst = v; }
+
+// d_eps of the whole batch: the groups' partial sums added in group order (fixed, deterministic)
+__global__ void sum_groups_kernel(double* parts, int n) {
+    double s = 0.0;
+    for (int g = 0; g < n; ++g) s += parts[1 + g];
+    parts[0] = s;
+}
 
 static onedf_status finish(cudaError_t e) {
     if (e != cudaSuccess) { cudaGetLastError(); return ONEDF_ERR_CUDA; }
@@ -289,33 +300,80 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
     StepLayout L = step_layout(p, ws);
     void* sub = (char*)ws + L.sub_off;
     const int64_t BH = p->B * p->H, N = p->N;
-    const size_t bk = (size_t)(BH * N * p->d_k) * 4, bv = (size_t)(BH * N * p->d_v) * 4;
-    cudaError_t e = cudaMemsetAsync(ws, 0, 4, st);
+    const int G = (int)min64(BH, STEP_GROUPS_MAX);
+    // side streams for the copies; events order them against the compute on `st`
+    cudaStream_t sin = nullptr, sout = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_in[STEP_GROUPS_MAX] = {}, ev_c[STEP_GROUPS_MAX] = {};
+    cudaError_t e = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming);
+    for (int g = 0; g < G && e == cudaSuccess; ++g) {
+        e = cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_c[g], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(ws, 0, 4, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(sub, 0, 4, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(L.Q, Q_h, bk, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(L.K, K_h, bk, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(L.V, V_h, bv, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(L.dO, dO_h, bv, cudaMemcpyHostToDevice, st);
     // eps by value: written by a one-thread kernel so the call needs no host staging buffer
     if (e == cudaSuccess) {
         set_scalar_kernel<<<1, 1, 0, st>>>(L.eps, eps);
         e = cudaGetLastError();
     }
-    if (e != cudaSuccess) return finish(e);
-    if ((s = do_encode(p, L.Q, L.K, nullptr, L.qcode, L.kcode, nullptr, sub, st, false)) != ONEDF_OK) return s;
-    if ((s = do_sort(p, L.kcode, L.scode, L.perm, sub, st)) != ONEDF_OK) return s;
-    if ((s = do_fwd(p, L.Q, L.K, L.V, L.eps, L.qcode, L.scode, L.perm, L.O, L.idx, L.Z, sub, st, false)) != ONEDF_OK)
-        return s;
-    if ((s = do_bwd(p, L.Q, L.K, L.V, L.eps, L.O, L.dO, L.idx, L.Z, L.qcode, L.perm, L.dQ, L.dK, L.dV, L.d_eps, sub,
-                    st, false)) !=
-        ONEDF_OK)
-        return s;
-    e = cudaMemcpyAsync(ws, sub, 4, cudaMemcpyDeviceToDevice, st);   // surface device flags in the caller's header
-    if (e == cudaSuccess) e = cudaMemcpyAsync(O_h, L.O, bv, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dQ_h, L.dQ, bk, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dK_h, L.dK, bk, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(dV_h, L.dV, bv, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_eps_h, L.d_eps, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_start, st);       // prior work on `st` precedes the copies
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, ev_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev_start, 0);
+    int64_t h0 = 0;
+    for (int g = 0; g < G && e == cudaSuccess; ++g) {
+        const int64_t nh = BH / G + (g < BH % G ? 1 : 0);           // slices of group g: [h0, h0 + nh)
+        onedf_problem pg = *p;
+        pg.B = 1;
+        pg.H = nh;
+        const size_t ok = (size_t)(h0 * N * p->d_k), ov = (size_t)(h0 * N * p->d_v), o1 = (size_t)(h0 * N);
+        const size_t bk = (size_t)(nh * N * p->d_k) * 4, bv = (size_t)(nh * N * p->d_v) * 4;
+        e = cudaMemcpyAsync(L.Q + ok, Q_h + ok, bk, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(L.K + ok, K_h + ok, bk, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(L.V + ov, V_h + ov, bv, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(L.dO + ov, dO_h + ov, bv, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_in[g], sin);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_in[g], 0);
+        if (e != cudaSuccess) break;
+        if ((s = do_encode(&pg, L.Q + ok, L.K + ok, nullptr, L.qcode + o1, L.kcode + o1, nullptr, sub, st, false)) !=
+            ONEDF_OK)
+            break;
+        if ((s = do_sort(&pg, L.kcode + o1, L.scode + o1, L.perm + o1, sub, st)) != ONEDF_OK) break;
+        if ((s = do_fwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.qcode + o1, L.scode + o1, L.perm + o1, L.O + ov,
+                        L.idx + o1 * p->k, L.Z + o1, sub, st, false)) != ONEDF_OK)
+            break;
+        if ((s = do_bwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.O + ov, L.dO + ov, L.idx + o1 * p->k, L.Z + o1,
+                        L.qcode + o1, L.perm + o1, L.dQ + ok, L.dK + ok, L.dV + ov, L.d_eps + 1 + g, sub, st,
+                        false)) != ONEDF_OK)
+            break;
+        e = cudaEventRecord(ev_c[g], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev_c[g], 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(O_h + ov, L.O + ov, bv, cudaMemcpyDeviceToHost, sout);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dQ_h + ok, L.dQ + ok, bk, cudaMemcpyDeviceToHost, sout);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dK_h + ok, L.dK + ok, bk, cudaMemcpyDeviceToHost, sout);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dV_h + ov, L.dV + ov, bv, cudaMemcpyDeviceToHost, sout);
+        h0 += nh;
+    }
+    if (s == ONEDF_OK && e == cudaSuccess) {
+        sum_groups_kernel<<<1, 1, 0, st>>>(L.d_eps, G);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaMemcpyAsync(ws, sub, 4, cudaMemcpyDeviceToDevice, st);   // surface device flags
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_eps_h, L.d_eps, 8, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_end, sout);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end, 0);      // the caller's stream covers all copies
+    }
+    // streams/events are released once their pending work completes (no synchronisation here)
+    for (int g = 0; g < G; ++g) {
+        if (ev_in[g]) cudaEventDestroy(ev_in[g]);
+        if (ev_c[g]) cudaEventDestroy(ev_c[g]);
+    }
+    if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_end) cudaEventDestroy(ev_end);
+    if (sin) cudaStreamDestroy(sin);
+    if (sout) cudaStreamDestroy(sout);
+    if (s != ONEDF_OK) return s;
     return finish(e);
 }
 

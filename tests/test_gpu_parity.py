@@ -346,3 +346,28 @@ def test_schedule_hints_do_not_change_results(name):
     b = [v.cpu().numpy() for v in b]
     for u, v, n in zip(a, b, ("dQ", "dK", "dV", "d_eps")):
         assert np.array_equal(np.atleast_1d(u).view(np.uint8), np.atleast_1d(v).view(np.uint8)), n
+
+
+def test_host_step_pipelined_groups_match_device_path():
+    """onedf_topk_attn_step_host pipelines groups of (b,h) slices over three streams; every
+    slice's outputs are the device path's bit for bit (slices are independent), d_eps is the
+    groups' partial sums added in order (within tolerance of the single-call reduction)."""
+    import torch
+
+    import paper_2501_14577_b200 as onedf
+    kw = dict(B=2, H=5, N=1024, d_k=3, d_v=32, k=16, window=32, chunk=128, causal=1, mean_slot=1)
+    rng = np.random.default_rng(8)
+    x = {n: rng.normal(size=(2, 5, 1024, w)).astype(np.float32) for n, w in (("Q", 3), ("K", 3), ("V", 32),
+                                                                               ("dO", 32))}
+    ref = gpu_run(kw, x)
+    p = onedf.make_problem(**kw)
+    hs = onedf.HostStep(p, torch.device("cuda:0"))
+    pin = {n: torch.from_numpy(v).pin_memory() for n, v in x.items()}
+    outs = {n: torch.empty_like(pin["V" if n in ("O", "dV") else "Q"]).pin_memory() for n in ("O", "dQ", "dK", "dV")}
+    d_eps = torch.zeros((), dtype=torch.float64).pin_memory()
+    for _ in range(2):                                   # the second call reuses the workspace
+        hs(pin["Q"], pin["K"], pin["V"], synth.EPS, pin["dO"], outs["O"], outs["dQ"], outs["dK"], outs["dV"], d_eps)
+        torch.cuda.synchronize()
+        for n in ("O", "dQ", "dK", "dV"):
+            assert np.array_equal(outs[n].numpy(), ref[n]), n
+        assert float(d_eps) == pytest.approx(float(ref["d_eps"]), rel=1e-12)
