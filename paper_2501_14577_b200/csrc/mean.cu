@@ -53,8 +53,9 @@ struct ScanSrc {
     double kt = 1.0;      // MODE 1: w (q - kt Kbar); 0 for the DOT score (dKbar = w q)
 };
 
+// inv = 1/(i+1) for the causal scans (A11's weights), from the tile's table; 1 otherwise
 template <int MODE>
-__device__ __forceinline__ double scan_value(const ScanSrc& s, int64_t bh, int64_t N, int64_t i, int c) {
+__device__ __forceinline__ double scan_value(const ScanSrc& s, int64_t bh, int64_t N, int64_t i, int c, double inv) {
     const int64_t row = bh * N + i;
     if (MODE == 0) return (double)__ldg(s.X + row * s.C + c);
     const float2 mc = __ldg(s.muco + row);
@@ -65,7 +66,31 @@ __device__ __forceinline__ double scan_value(const ScanSrc& s, int64_t bh, int64
     } else {
         y = (double)mc.x * (double)__ldg(s.X + row * s.C + c);
     }
-    return s.causal ? y / (double)(i + 1) : y;
+    return s.causal ? y * inv : y;
+}
+
+constexpr int SCAN_UNROLL = 8;        // rows loaded ahead per thread (independent loads in flight)
+
+// 1/(r+1) for the tile's rows, once per CTA (the divisor is shared by every column)
+__device__ __forceinline__ void fill_inv(double* s_inv, int64_t tile) {
+    for (int t = threadIdx.x; t < SCAN_TB; t += blockDim.x) s_inv[t] = 1.0 / (double)(tile * SCAN_TB + t + 1);
+}
+
+// sum of the thread's rows [r0, r1), loads batched SCAN_UNROLL at a time, fixed order
+template <int MODE>
+__device__ __forceinline__ double rows_sum(const ScanSrc& s, int64_t bh, int64_t N, int64_t r0, int64_t r1, int c,
+                                           const double* s_inv, int64_t tbase) {
+    double acc = 0.0;
+    int64_t r = r0;
+    for (; r + SCAN_UNROLL <= r1; r += SCAN_UNROLL) {
+        double v[SCAN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) v[u] = scan_value<MODE>(s, bh, N, r + u, c, s_inv[r + u - tbase]);
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) acc += v[u];
+    }
+    for (; r < r1; ++r) acc += scan_value<MODE>(s, bh, N, r, c, s_inv[r - tbase]);
+    return acc;
 }
 
 // (1) tile sums -> part[bh][tile][c]
@@ -73,13 +98,17 @@ template <int MODE>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_tile_sums_kernel(const ScanSrc s, int64_t N, int64_t ntile,
                                                                       int CW, double* __restrict__ part) {
     __shared__ double sh[SCAN_THREADS];
+    __shared__ double s_inv[SCAN_TB];
     const int64_t bh = blockIdx.y, tile = blockIdx.x;
     const int c = threadIdx.x % CW, g = threadIdx.x / CW, RG = SCAN_THREADS / CW;
     const int per = SCAN_TB / RG;
     const int64_t r0 = tile * SCAN_TB + (int64_t)g * per, r1 = min64(N, r0 + per);
+    if (MODE != 0) {
+        fill_inv(s_inv, tile);
+        __syncthreads();
+    }
     double acc = 0.0;
-    if (c < s.C)
-        for (int64_t r = r0; r < r1; ++r) acc += scan_value<MODE>(s, bh, N, r, c);
+    if (c < s.C) acc = rows_sum<MODE>(s, bh, N, r0, r1, c, s_inv, tile * SCAN_TB);
     sh[threadIdx.x] = acc;
     __syncthreads();
     if (g == 0 && c < s.C) {
@@ -111,22 +140,35 @@ __global__ void __launch_bounds__(SCAN_THREADS) mean_apply_kernel(const ScanSrc 
                                                                   const double* __restrict__ part,
                                                                   float* __restrict__ out) {
     __shared__ double sh[SCAN_THREADS];
+    __shared__ double s_inv[SCAN_TB];
     const int64_t bh = blockIdx.y, tile = blockIdx.x;
     const int c = threadIdx.x % CW, g = threadIdx.x / CW, RG = SCAN_THREADS / CW;
     const int per = SCAN_TB / RG;
     const int64_t r0 = tile * SCAN_TB + (int64_t)g * per, r1 = min64(N, r0 + per);
+    const int64_t tb = tile * SCAN_TB;
+    fill_inv(s_inv, tile);
     const bool on = c < s.C;
     double own = 0.0;
-    if (on)
-        for (int64_t r = r0; r < r1; ++r) own += scan_value<0>(s, bh, N, r, c);
+    if (on) own = rows_sum<0>(s, bh, N, r0, r1, c, s_inv, tb);
     sh[threadIdx.x] = own;
     __syncthreads();
     if (!on) return;
     double run = part[(bh * (ntile + 1) + tile) * s.C + c];
     for (int x = 0; x < g; ++x) run += sh[x * CW + c];
-    for (int64_t r = r0; r < r1; ++r) {
-        run += scan_value<0>(s, bh, N, r, c);
-        out[(bh * N + r) * s.C + c] = (float)(run / (double)(r + 1));
+    int64_t r = r0;
+    for (; r + SCAN_UNROLL <= r1; r += SCAN_UNROLL) {
+        double v[SCAN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) v[u] = scan_value<0>(s, bh, N, r + u, c, 1.0);
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) {
+            run += v[u];
+            out[(bh * N + r + u) * s.C + c] = (float)(run * s_inv[r + u - tb]);
+        }
+    }
+    for (; r < r1; ++r) {
+        run += scan_value<0>(s, bh, N, r, c, 1.0);
+        out[(bh * N + r) * s.C + c] = (float)(run * s_inv[r - tb]);
     }
 }
 
@@ -144,10 +186,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) grad_apply_kernel(const ScanSrc 
                                                                   const double* __restrict__ part,
                                                                   float* __restrict__ D) {
     __shared__ double sh[SCAN_THREADS];
+    __shared__ double s_inv[SCAN_TB];
     const int64_t bh = blockIdx.y, tile = blockIdx.x;
     const int c = threadIdx.x % CW, g = threadIdx.x / CW, RG = SCAN_THREADS / CW;
     const int per = SCAN_TB / RG;
     const int64_t r0 = tile * SCAN_TB + (int64_t)g * per, r1 = min64(N, r0 + per);
+    const int64_t tb = tile * SCAN_TB;
     const bool on = c < s.C;
     if (!s.causal) {
         if (!on) return;
@@ -158,16 +202,32 @@ __global__ void __launch_bounds__(SCAN_THREADS) grad_apply_kernel(const ScanSrc 
         }
         return;
     }
+    fill_inv(s_inv, tile);
+    __syncthreads();
     double own = 0.0;
-    if (on)
-        for (int64_t r = r0; r < r1; ++r) own += scan_value<MODE>(s, bh, N, r, c);
+    if (on) own = rows_sum<MODE>(s, bh, N, r0, r1, c, s_inv, tb);
     sh[threadIdx.x] = own;
     __syncthreads();
     if (!on) return;
     double run = part[(bh * (ntile + 1) + tile) * s.C + c];    // sum over later tiles
     for (int x = RG - 1; x > g; --x) run += sh[x * CW + c];      // later row-groups of this tile
-    for (int64_t r = r1 - 1; r >= r0; --r) {
-        run += scan_value<MODE>(s, bh, N, r, c);
+    int64_t r = r1 - 1;
+    for (; r - SCAN_UNROLL + 1 >= r0; r -= SCAN_UNROLL) {
+        double v[SCAN_UNROLL];
+        float d[SCAN_UNROLL];
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) {
+            v[u] = scan_value<MODE>(s, bh, N, r - u, c, s_inv[r - u - tb]);
+            d[u] = D[(bh * N + r - u) * s.C + c];
+        }
+#pragma unroll
+        for (int u = 0; u < SCAN_UNROLL; ++u) {
+            run += v[u];
+            D[(bh * N + r - u) * s.C + c] = (float)((double)d[u] + run);
+        }
+    }
+    for (; r >= r0; --r) {
+        run += scan_value<MODE>(s, bh, N, r, c, s_inv[r - tb]);
         float* o = D + (bh * N + r) * s.C + c;
         *o = (float)((double)*o + run);
     }
