@@ -16,16 +16,19 @@
 //      window w = min(W, len), s = clamp(p - W/2) (D1, D2).
 //  A6  the warp streams every window as contiguous 16/32/48-B key records
 //      (coords + original position, built by K4 in sorted order, so a window
-//      is one coalesced burst), ranks each candidate by the f32 distance in
+//      is one coalesced burst) and ranks each candidate by the f32 distance in
 //      the pinned order (D23) packed with its position into a u64 key
-//      (D bits << 32 | j; D >= 0 so the bit pattern is order-preserving), and
-//      keeps the exact top-k in REGISTERS: the running top-KC list is spread
-//      over the warp (KC/32 keys per lane, element e = r*32 + lane, ascending
-//      in e).  Keys below the current k-th key are appended (ballot + popc
-//      compaction) to a 32-entry pending list; a full list is bitonic-sorted
-//      across the lanes with xor-shuffles, reversed, min-merged into the top
-//      list's last row (the lowest KC of both form a bitonic sequence) and a
-//      half-cleaner cascade (register and shuffle stages) restores order.
+//      (D bits << 32 | j; D >= 0 so the bit pattern is order-preserving).
+//      Two passes: (1) per-lane f32 min-lists of length 2*ceil(k/32) give a
+//      bound T with #{D <= T} >= k (bisection over the union of the lists);
+//      (2) every candidate with D <= T is appended to a per-warp shared-memory
+//      buffer (integer cursor; ~1.4 k keys on average).  The collected keys
+//      are unique, so their order is fixed by the keys alone: each 32-key row
+//      is bitonic-sorted across the lanes with xor-shuffles, reversed,
+//      min-merged into the register top list's last row (the lowest 32R of
+//      both form a bitonic sequence) and a half-cleaner cascade restores
+//      order.  If more than FWD_CAP keys tie at or below T, a streaming
+//      selection with the same merges takes over.
 //  A7  S = 1/(D + eps) in f64, mean slot from the prefix means (D8), Z by a
 //      fixed-order warp tree, and o = sum A v + A_mu Vbar with f64
 //      accumulators; V rows are gathered as float4 bursts (16 lanes per
@@ -49,9 +52,6 @@ constexpr int FWD_THREADS = FWD_WARPS * 32;
 #endif
 #ifndef ONEDF_FWD_COLLECT
 #define ONEDF_FWD_COLLECT 1          // pass-2 append: 0 ballot + popc compaction, 1 shared-memory atomic cursor
-#endif
-#ifndef ONEDF_FWD_RANK
-#define ONEDF_FWD_RANK 0             // order of the collected keys: 0 rank counting, 1 register bitonic sort
 #endif
 constexpr int FWD_QPW = ONEDF_FWD_QPW;              // queries per warp (schedule stretch per CTA = 8*QPW)
 constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 loaded ahead (W = 128 -> one window)
@@ -126,18 +126,6 @@ __device__ __forceinline__ unsigned long long list_get(const unsigned long long 
 #pragma unroll
     for (int r = 1; r < R; ++r) v = (e >> 5) == r ? top[r] : v;
     return __shfl_sync(FULL, v, e & 31);
-}
-
-// The first 32*RO keys (ascending) of buf[0..cnt) (unique keys), sorted as 32*RS.
-template <int RS, int RO>
-__device__ __forceinline__ void sort_collected(const unsigned long long* buf, int cnt, unsigned long long (&top)[RO]) {
-    const int lane = lane_id();
-    unsigned long long x[RS];
-#pragma unroll
-    for (int r = 0; r < RS; ++r) x[r] = r * 32 + lane < cnt ? buf[r * 32 + lane] : KEY_MAX;
-    warp_sort<RS>(x);
-#pragma unroll
-    for (int r = 0; r < RO; ++r) top[r] = r < RS ? x[r] : KEY_MAX;
 }
 
 #ifdef ONEDF_FWD_STATS
@@ -259,11 +247,9 @@ template <int DK, int R>
 __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_kernel(const FwdArgs a) {
     constexpr int L = PassOne<R>::L;
     __shared__ __align__(16) unsigned long long s_buf[FWD_WARPS][FWD_CAP + 32 * FWD_UB];
-    __shared__ __align__(16) unsigned long long s_top[FWD_WARPS][32 * R];
     __shared__ int s_cnt[FWD_WARPS];
     const int warp = threadIdx.x / 32, lane = lane_id();
     unsigned long long* buf = s_buf[warp];
-    unsigned long long* stop = s_top[warp];
     const float e = __ldg(a.eps);
     if (a.score == SC_CAUCHY && blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e)))
         set_flag(a.ws, FLAG_BAD_EPS);
@@ -388,35 +374,12 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         __syncwarp();
         unsigned long long top[R];
         if (fits) {
-#if ONEDF_FWD_RANK == 1
-            // ---------------- exact order of the collected keys: register bitonic sort
-            if (cnt <= 32 * R) sort_collected<R, R>(buf, cnt, top);
-            else if (cnt <= 64 * R) sort_collected<(2 * R > 8 ? 8 : 2 * R), R>(buf, cnt, top);
-            else if (cnt <= 128 * R || R >= 4) sort_collected<(4 * R > 8 ? 8 : 4 * R), R>(buf, cnt, top);
-            else sort_collected<8, R>(buf, cnt, top);
-#else
-            // ---------------- exact order of the collected keys by counting (keys are unique)
-            for (int t = lane; t < 32 * R; t += 32) stop[t] = KEY_MAX;
-            __syncwarp();
-            // each lane ranks its elements e = m*32 + lane against all cnt keys
-            const int mm = (cnt + 31) / 32;
-            for (int m = 0; m < mm; ++m) {
-                const int e2 = m * 32 + lane;
-                const unsigned long long mine = e2 < cnt ? buf[e2] : KEY_MAX;
-                int rank = 0;
-                const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(buf);
-                int x = 0;
-                for (; x + 4 <= cnt; x += 4) {
-                    const ulonglong2 y0 = b2[x / 2], y1 = b2[x / 2 + 1];
-                    rank += (y0.x < mine) + (y0.y < mine) + (y1.x < mine) + (y1.y < mine);
-                }
-                for (; x < cnt; ++x) rank += buf[x] < mine;
-                if (e2 < cnt && rank < k) stop[rank] = mine;
-            }
-            __syncwarp();
+            // ---------------- exact order of the collected keys: 32-key rows merged into the
+            // register top list (shuffle bitonic sort of the row + min-merge + half-cleaners)
 #pragma unroll
-            for (int r = 0; r < R; ++r) top[r] = stop[r * 32 + lane];
-#endif
+            for (int r = 0; r < R; ++r) top[r] = KEY_MAX;
+            for (int m = 0; m * 32 < cnt; ++m)
+                merge_pending<R>(top, m * 32 + lane < cnt ? buf[m * 32 + lane] : KEY_MAX);
         } else {
             // ---------------- rare: too many keys at or below T (e.g. many equal
             // distances) -- streaming selection with shuffle-bitonic merges,
