@@ -39,7 +39,8 @@ class _Problem(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int64), ("H", ctypes.c_int64), ("N", ctypes.c_int64),
                 ("d_k", ctypes.c_int32), ("d_v", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("window", ctypes.c_int32), ("chunk", ctypes.c_int32), ("bits", ctypes.c_int32),
-                ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32), ("score", ctypes.c_int32)]
+                ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32), ("score", ctypes.c_int32),
+                ("select", ctypes.c_int32)]
 
 
 @dataclass
@@ -56,6 +57,7 @@ class Problem:
     causal: int = 1
     mean_slot: int = 1
     score: int = 0         # 0 Cauchy (Eq. 5); 1 neg-Euclidean exp, 2 inverse Euclidean, 3 dot product (D24)
+    select: int = 0        # 0 Euclidean top-k of the windows (D5); 1 SPEC's code-distance merge (D25)
 
     @property
     def BH(self) -> int:
@@ -71,11 +73,11 @@ class Problem:
 
     def c(self) -> _Problem:
         return _Problem(self.B, self.H, self.N, self.d_k, self.d_v, self.k, self.window, self.chunk,
-                        self.bits, self.causal, self.mean_slot, self.score)
+                        self.bits, self.causal, self.mean_slot, self.score, self.select)
 
     def slice(self, n_bh: int) -> "Problem":
         return Problem(1, n_bh, self.N, self.d_k, self.d_v, self.k, self.window, self.chunk, self.bits,
-                       self.causal, self.mean_slot, self.score)
+                       self.causal, self.mean_slot, self.score, self.select)
 
 
 _lib = None
@@ -103,6 +105,7 @@ def lib():
             "oref_bruteforce_knn": (ctypes.c_int, [P, vp, vp, vp]),
             "oref_forward_score": (ctypes.c_int, [P, vp, vp, vp, vp, vp, vp]),
             "oref_code_knn": (ctypes.c_int, [P, vp, vp, ctypes.c_int, vp]),
+            "oref_select_code": (ctypes.c_int, [P, vp, vp, vp, vp]),
             "oref_backward_score": (ctypes.c_int, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "oref_num_threads": (ctypes.c_int, []),
         }
@@ -202,6 +205,12 @@ def select(p: Problem, Q, K, qcode, scode, perm, sel=None):
     """Top-k index sets; all queries -> [B,H,N,k], else [len(sel), k] for flat ids bh*N+i."""
     Q = _c(Q, np.float32); K = _c(K, np.float32)
     qcode = _c(qcode, np.uint64); scode = _c(scode, np.uint64); perm = _c(perm, np.int32)
+    if p.select:
+        # SPEC's code-distance merge (D25): all queries
+        assert sel is None, "code-distance selection: all queries only"
+        idx = np.zeros((p.B, p.H, p.N, p.k), dtype=np.int32)
+        _check(lib().oref_select_code(ctypes.byref(p.c()), _ptr(qcode), _ptr(scode), _ptr(perm), _ptr(idx)))
+        return idx
     n, s = _sel(sel)
     shape = (p.B, p.H, p.N, p.k) if s is None else (n, p.k)
     idx = np.zeros(shape, dtype=np.int32)

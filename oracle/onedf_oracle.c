@@ -45,6 +45,7 @@ typedef struct {
     int32_t causal;
     int32_t mean_slot;
     int32_t score;      /* 0 Cauchy (Eq. 5); 1..3 the comparison operators (reading D24) */
+    int32_t select;     /* 0 Euclidean top-k of the windows (D5); 1 SPEC's code-distance merge (D25) */
 } oref_problem;
 
 enum { OREF_OK = 0, OREF_ERR_INVALID_ARG = 1, OREF_ERR_NONFINITE = 4 };
@@ -265,6 +266,57 @@ static int select_one(const oref_problem* p, int64_t bh, int64_t i, const float*
     int nk = nc < k ? (int)nc : k;
     for (int r = 0; r < k; ++r) idx_row[r] = r < nk ? buf[r].j : -1;
     return nk;
+}
+
+/* Selection variant (reading D25): SPEC's query_topk
+ * (S:224-228): the same per-run windows (steps 5, D1-D3), "merged across
+ * chunks by |code - query_code| with ties broken by smaller source_index";
+ * the first min(k, |C_i|) candidates by (|scode - qcode| as u64, j).        */
+typedef struct { uint64_t d; int32_t j; } code_cand2;
+static int cmp_code_cand2(const void* a, const void* b) {
+    const code_cand2* x = (const code_cand2*)a; const code_cand2* y = (const code_cand2*)b;
+    if (x->d != y->d) return x->d < y->d ? -1 : 1;
+    return (x->j > y->j) - (x->j < y->j);
+}
+
+static void select_one_code(const oref_problem* p, int64_t bh, int64_t i, const uint64_t* qcode,
+                            const uint64_t* scode, const int32_t* perm, code_cand2* buf, int32_t* idx_row) {
+    const int64_t N = p->N;
+    const int W = eff_window(p), k = p->k;
+    const int64_t nruns = p->causal ? i / p->chunk : 1;
+    const uint64_t qc = qcode[bh * N + i];
+    int64_t nc = 0;
+    for (int64_t c = 0; c < nruns; ++c) {
+        int64_t s0, len;
+        run_span(p, c, &s0, &len);
+        const uint64_t* run = scode + bh * N + s0;
+        int64_t s, w;
+        oref_window_span(oref_insertion_point(run, len, qc), len, W, &s, &w);
+        for (int64_t r = s; r < s + w; ++r) {
+            const uint64_t kc = run[r];
+            buf[nc].d = kc > qc ? kc - qc : qc - kc;
+            buf[nc].j = perm[bh * N + s0 + r];
+            ++nc;
+        }
+    }
+    qsort(buf, (size_t)nc, sizeof(code_cand2), cmp_code_cand2);
+    for (int r = 0; r < k; ++r) idx_row[r] = r < nc ? buf[r].j : -1;
+}
+
+int oref_select_code(const oref_problem* p, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,
+                     int32_t* idx) {
+    const int64_t BH = p->B * p->H, N = p->N;
+    const int W = eff_window(p);
+    if (p->k < 1 || W < p->k || (p->causal && p->chunk < 1)) return OREF_ERR_INVALID_ARG;
+    const int64_t maxc = (p->causal ? run_count(p) : 1) * (int64_t)W;
+    #pragma omp parallel
+    {
+        code_cand2* buf = (code_cand2*)malloc(sizeof(code_cand2) * (size_t)(maxc + 1));
+        #pragma omp for schedule(dynamic, 64)
+        for (int64_t t = 0; t < BH * N; ++t) select_one_code(p, t / N, t % N, qcode, scode, perm, buf, idx + t * p->k);
+        free(buf);
+    }
+    return OREF_OK;
 }
 
 /* Selection for every query (sel == NULL) or for the n_sel flat query ids

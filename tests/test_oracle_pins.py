@@ -627,3 +627,41 @@ def test_code_knn_ties_and_causality():
     assert idx[0, 0, 9].tolist() == [0, 1, 2]                # keys 0..7: five at d = 0, smallest j first
     qc[0, 0, 11] = 2
     assert oracle.code_knn(p, qc, kc)[0, 0, 11].tolist() == [4, 7, 0]   # d = 1 (key 4), 2 (key 7), then 3 (j = 0)
+
+
+# --------------------------------------------------------------------------- selection variant (NEXT-2, D25)
+def test_select_code_spec_examples():
+    """SPEC S:230-232 worked examples of query_topk (W = k = 2): run [1,3,5,7], query code 4 in
+    chunk 1 -> {3,5}; a query code below a whole run [5,6,9] -> {5,6}; chunk-0 query -> empty."""
+    p = Problem(1, 1, 8, 1, 4, 2, window=2, chunk=4, causal=1, mean_slot=0, select=1)
+    scode = np.array([[[1, 3, 5, 7, 0, 0, 0, 0]]], np.uint64)
+    perm = np.array([[[0, 1, 2, 3, 4, 5, 6, 7]]], np.int32)
+    qcode = np.array([[[0, 0, 0, 0, 4, 4, 0, 0]]], np.uint64)
+    idx = oracle.select(p, None, None, qcode, scode, perm)
+    assert sorted(scode[0, 0, idx[0, 0, 4]].tolist()) == [3, 5]
+    assert idx[0, 0, 0].tolist() == [-1, -1]
+    p2 = Problem(1, 1, 6, 1, 4, 2, window=2, chunk=3, causal=1, mean_slot=0, select=1)
+    idx2 = oracle.select(p2, None, None, np.zeros((1, 1, 6), np.uint64),
+                         np.array([[[5, 6, 9, 0, 0, 0]]], np.uint64), np.arange(6, dtype=np.int32)[None, None])
+    assert idx2[0, 0, 3].tolist() == [0, 1]                   # codes {5, 6}: window clamped at the run start
+
+
+def test_select_code_invariants_and_d1_exactness():
+    """Causality and |I| = min(k, admissible); the order is (|code difference|, j); S:257 d_K = 1
+    with unique codes and a window covering each run -> the exact chunk-causal kNN."""
+    rng = np.random.default_rng(60)
+    N, k, M = 256, 8, 32
+    X = rng.normal(size=(1, 1, N, 1)).astype(np.float32)
+    Qx = rng.normal(size=(1, 1, N, 1)).astype(np.float32)
+    p = Problem(1, 1, N, 1, 4, k, window=M, chunk=M, causal=1, mean_slot=0, select=1)
+    qc, kc, _ = oracle.encode(p, Qx, X)
+    sc, pm = oracle.sort(p, kc)
+    idx = oracle.select(p, Qx, X, qc, sc, pm)
+    exact = oracle.bruteforce_knn(p, Qx, X)
+    for i in range(N):
+        lim = (i // M) * M
+        row = [j for j in idx[0, 0, i] if j >= 0]
+        assert len(row) == min(k, lim) and all(j < lim for j in row)
+        d = [abs(int(kc[0, 0, j]) - int(qc[0, 0, i])) for j in row]
+        assert d == sorted(d)
+        assert set(row) == set(j for j in exact[0, 0, i] if j >= 0)
