@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define ONEDF_VERSION 400
+#define ONEDF_VERSION 500
 
 typedef struct CUstream_st* onedf_stream_t;   /* == cudaStream_t */
 
@@ -82,6 +82,9 @@ typedef struct {
                          /*   ONEDF_SCORE_CAUCHY 1/(D + eps) (Eq. 5, the method)        */
                          /*   ONEDF_SCORE_NEG_EUCLID exp(-D), ONEDF_SCORE_INV_EUCLID    */
                          /*   1/(sqrt(D) + 1e-6), ONEDF_SCORE_DOT exp(q.k / sqrt(d_k))  */
+    int32_t select;      /* index set of a query (reading D25): ONEDF_SELECT_EUCLID the */
+                         /*   exact Euclidean top-k of the candidate windows (D5, the   */
+                         /*   method); ONEDF_SELECT_CODE SPEC's code-distance merge      */
 } onedf_problem;
 
 /* Score variants: the paper's comparison operators
@@ -92,6 +95,12 @@ typedef struct {
  * (the log-sum-exp) for NEG_EUCLID and DOT; eps is read only by CAUCHY and
  * d_eps is 0 for the others. */
 enum { ONEDF_SCORE_CAUCHY = 0, ONEDF_SCORE_NEG_EUCLID = 1, ONEDF_SCORE_INV_EUCLID = 2, ONEDF_SCORE_DOT = 3 };
+
+/* Selection variant (SPEC S:224-228 query_topk): the same
+ * per-run windows (D1-D3), candidates ordered by (|scode - qcode| as u64, j)
+ * instead of (D32, j); idx is emitted in that order.  Everything downstream
+ * (weights, gather, backward) is unchanged. */
+enum { ONEDF_SELECT_EUCLID = 0, ONEDF_SELECT_CODE = 1 };
 
 enum {
     ONEDF_OP_ENCODE = 0,

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("ONEDF_LIB") or os.path.join(_PKG, "libonedf.so")
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NONFINITE, ERR_WORKSPACE = range(6)
 OP_ENCODE, OP_SORT, OP_FWD, OP_BWD, OP_STEP_HOST = range(5)
 SCORE_CAUCHY, SCORE_NEG_EUCLID, SCORE_INV_EUCLID, SCORE_DOT = range(4)
+SELECT_EUCLID, SELECT_CODE = range(2)
 
 
 class OnedfError(RuntimeError):
@@ -33,7 +34,8 @@ class Problem(ctypes.Structure):
                 ("d_k", ctypes.c_int32), ("d_v", ctypes.c_int32), ("k", ctypes.c_int32),
                 ("window", ctypes.c_int32), ("chunk", ctypes.c_int32), ("bits", ctypes.c_int32),
                 ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32),
-                ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32), ("score", ctypes.c_int32)]
+                ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32), ("score", ctypes.c_int32),
+                ("select", ctypes.c_int32)]
 
     def __repr__(self):
         return "Problem(" + ", ".join(f"{n}={getattr(self, n)}" for n, _ in self._fields_) + ")"

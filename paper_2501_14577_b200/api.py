@@ -11,8 +11,8 @@ from .abi import Problem
 
 
 def make_problem(B, H, N, d_k, d_v, k, window=0, chunk=1, bits=0, causal=1, mean_slot=1, shard_rank=0,
-                 shard_world=1, score=0) -> Problem:
-    p = Problem(B, H, N, d_k, d_v, k, window, chunk, bits, causal, mean_slot, shard_rank, shard_world, score)
+                 shard_world=1, score=0, select=0) -> Problem:
+    p = Problem(B, H, N, d_k, d_v, k, window, chunk, bits, causal, mean_slot, shard_rank, shard_world, score, select)
     st = abi.onedf_validate(p)
     if st != abi.OK:
         raise abi.OnedfError(st, "onedf_validate")

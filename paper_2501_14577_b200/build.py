@@ -2,6 +2,7 @@
 from __future__ import annotations
 
 import concurrent.futures
+import hashlib
 import os
 import subprocess
 import sys
@@ -27,6 +28,24 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _stamp(files, defines) -> str:
+    """Content hash of the sources, headers and flags a library is built from."""
+    h = hashlib.sha256()
+    for f in sorted(files):
+        with open(f, "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    h.update(" ".join(ARCH + FLAGS + list(defines)).encode())
+    return h.hexdigest()
+
+
+def _read(path: str):
+    try:
+        with open(path) as f:
+            return f.read()
+    except OSError:
+        return None
+
+
 def _headers():
     hs = [os.path.join(INCLUDE, "onedf.h")]
     hs += [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
@@ -38,8 +57,9 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     os.makedirs(objdir, exist_ok=True)
     hdrs = _headers()
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    if not force and not defines and not _stale(lib, srcs + hdrs):
-        return lib          # the library is newer than every source (objects need not be present)
+    stamp = _stamp(srcs + hdrs, defines)
+    if not force and not defines and _read(lib + ".stamp") == stamp and os.path.exists(lib):
+        return lib          # built from exactly these sources and flags (objects need not be present)
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
@@ -62,10 +82,13 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
             if verbose and log:
                 sys.stderr.write(log)
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _stale(lib, objs):
+    if force or jobs or _stale(lib, objs) or _read(lib + ".stamp") != stamp:
         cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"]
         subprocess.run(cmd, check=True)
         os.replace(lib + ".tmp", lib)
+    if not defines and _stamp(srcs + hdrs, defines) == stamp:   # sources unchanged while compiling
+        with open(lib + ".stamp", "w") as f:
+            f.write(stamp)
     return lib
 
 

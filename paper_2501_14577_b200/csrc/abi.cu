@@ -58,6 +58,7 @@ static onedf_status validate(const onedf_problem* p) {
     if (p->N * (int64_t)p->k >= (1ll << 31)) return ONEDF_ERR_INVALID_ARG;
     if (p->shard_world < 0 || p->shard_world > 4096) return ONEDF_ERR_INVALID_ARG;
     if (p->score < ONEDF_SCORE_CAUCHY || p->score > ONEDF_SCORE_DOT) return ONEDF_ERR_INVALID_ARG;
+    if (p->select != ONEDF_SELECT_EUCLID && p->select != ONEDF_SELECT_CODE) return ONEDF_ERR_INVALID_ARG;
     if (p->shard_world > 1) {
         if (p->shard_rank < 0 || p->shard_rank >= p->shard_world) return ONEDF_ERR_INVALID_ARG;
         if (!p->causal) return ONEDF_ERR_UNSUPPORTED;   // sequence sharding is defined over causal chunks

@@ -243,6 +243,115 @@ __device__ __forceinline__ unsigned long long make_key(float D, int j) {
 template <int R>
 struct PassOne { static constexpr int L = 2 * R; };
 
+// A7 for one query: weights (f64) of the selected keys jr[] (slot e = r*32 + lane,
+// -1 = empty) and the mean slot, the normaliser Z, and the value gather o.
+template <int DK, int R>
+__device__ __forceinline__ void attend_row(const FwdArgs& a, int64_t bh, int64_t i, int64_t gq, const float* q,
+                                           const int (&jr)[R], int nsel, double ed) {
+    const int lane = lane_id();
+    const int64_t N = a.N;
+    // ---------------- A7: weights (f64): Cauchy Eq. 5, or a score variant (D24)
+    const int sc = a.score;
+    double Sr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        Sr[r] = 0.0;
+        if (jr[r] >= 0) {
+            float kj[DK];
+#pragma unroll
+            for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + jr[r]) * DK + d);
+            Sr[r] = score_raw<DK>(sc, q, kj, ed);
+        }
+    }
+    double Smu = 0.0;
+    const int64_t mrow = a.causal ? i : 0;
+    if (a.mean_slot) {
+        float kb[DK];
+#pragma unroll
+        for (int d = 0; d < DK; ++d) kb[d] = __ldg(a.Kbar + (bh * (a.causal ? N : 1) + mrow) * DK + d);
+        Smu = score_raw<DK>(sc, q, kb, ed);
+    }
+    double xmax = 0.0;
+    if (score_is_exp(sc)) {
+        // softmax scores: shift by the largest logit (fixed-order warp max), S = exp(x - xmax)
+        double m = -INFINITY;
+#pragma unroll
+        for (int r = 0; r < R; ++r) m = jr[r] >= 0 ? fmax(m, Sr[r]) : m;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
+        if (a.mean_slot) m = fmax(m, Smu);
+        xmax = m;
+#pragma unroll
+        for (int r = 0; r < R; ++r) Sr[r] = jr[r] >= 0 ? exp(Sr[r] - xmax) : 0.0;
+        if (a.mean_slot) Smu = exp(Smu - xmax);
+    }
+    double zpart = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) zpart += Sr[r];
+    double Zi = warp_sum(zpart);
+    if (a.mean_slot) Zi += Smu;
+    const double invZ = Zi > 0.0 ? 1.0 / Zi : 0.0;
+
+    // ---------------- A7: value gather, float4 chunks, lane groups over slots
+    const int nch = a.dv / 4;
+    int P = 1;
+    while (P < nch && P < 32) P <<= 1;
+    const int G = 32 / P;                 // rows per step (1 when nch >= 32)
+    const int grp = lane / P, ch_l = lane % P;
+    const float* Vb = a.V + bh * N * (int64_t)a.dv;
+    float* orow = a.O + gq * (int64_t)a.dv;
+    const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)a.dv;
+    const double Amu = Smu * invZ;
+    for (int ch0 = 0; ch0 < nch; ch0 += P) {
+        const int ch = ch0 + ch_l;
+        const bool act = ch < nch;
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (r * 32 >= nsel) break;
+            for (int t0 = 0; t0 < 32 && r * 32 + t0 < nsel; t0 += 4 * G) {
+                float4 v4[4];
+                double A4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int src = (t0 + u * G + grp) & 31;
+                    const int j = __shfl_sync(FULL, jr[r], src);
+                    A4[u] = __shfl_sync(FULL, Sr[r], src) * invZ;
+                    const bool ok = act && t0 + u * G + grp < 32 && r * 32 + t0 + u * G + grp < nsel;
+                    v4[u] = ok ? __ldg(reinterpret_cast<const float4*>(Vb + (int64_t)j * a.dv) + ch)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (!ok) A4[u] = 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc0 = fma(A4[u], (double)v4[u].x, acc0);
+                    acc1 = fma(A4[u], (double)v4[u].y, acc1);
+                    acc2 = fma(A4[u], (double)v4[u].z, acc2);
+                    acc3 = fma(A4[u], (double)v4[u].w, acc3);
+                }
+            }
+        }
+        for (int o = P; o < 32; o <<= 1) {
+            acc0 += __shfl_xor_sync(FULL, acc0, o);
+            acc1 += __shfl_xor_sync(FULL, acc1, o);
+            acc2 += __shfl_xor_sync(FULL, acc2, o);
+            acc3 += __shfl_xor_sync(FULL, acc3, o);
+        }
+        if (grp == 0 && act) {
+            if (a.mean_slot) {
+                const float4 vb = __ldg(reinterpret_cast<const float4*>(vbar) + ch);
+                acc0 = fma(Amu, (double)vb.x, acc0);
+                acc1 = fma(Amu, (double)vb.y, acc1);
+                acc2 = fma(Amu, (double)vb.z, acc2);
+                acc3 = fma(Amu, (double)vb.w, acc3);
+            }
+            reinterpret_cast<float4*>(orow)[ch] =
+                make_float4((float)acc0, (float)acc1, (float)acc2, (float)acc3);
+        }
+    }
+    if (lane == 0) a.Z[gq] = (float)(score_is_exp(sc) ? (Zi > 0.0 ? xmax + log(Zi) : 0.0) : Zi);
+}
+
 template <int DK, int R>
 __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_kernel(const FwdArgs a) {
     constexpr int L = PassOne<R>::L;
@@ -433,106 +542,178 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
             nsel += __popc(__ballot_sync(FULL, valid));
         }
 
-        // ---------------- A7: weights (f64): Cauchy Eq. 5, or a score variant (D24)
-        const int sc = a.score;
-        double Sr[R];
+        attend_row<DK, R>(a, bh, i, gq, q, jr, nsel, ed);
+
+    }
+}
+
+// ------------------------------------------------------------------ selection variant (D25)
+// SPEC's query_topk: the same per-run windows, candidates ordered by
+// (|scode - qcode| as u64, j) -- NEXT-2's code-distance merge.  One warp per
+// query: (1) per-lane lists of the 2R smallest u64 distances bound the k-th
+// distance T (bisection over the union of the lists); (2) every candidate with
+// distance <= T is appended to shared memory and ranked by (distance, j) (the
+// pairs are unique); more than CODE_CAP such candidates (repeated codes) fall
+// back to k rounds of a warp-wide minimum above the last pair.  Then the same
+// A7 as the Euclidean path (attend_row).
+constexpr int CODE_CAP = 256;
+
+__device__ __forceinline__ bool pair_lt(unsigned long long d0, int j0, unsigned long long d1, int j1) {
+    return d0 < d1 || (d0 == d1 && j0 < j1);
+}
+
+template <int DK, int R>
+__global__ void __launch_bounds__(FWD_THREADS) code_select_attn_kernel(const FwdArgs a) {
+    constexpr int L = 2 * R;
+    constexpr int REC = RecW<DK>::value;
+    __shared__ unsigned long long s_d[FWD_WARPS][CODE_CAP];
+    __shared__ int s_j[FWD_WARPS][CODE_CAP];
+    __shared__ int s_cnt[FWD_WARPS];
+    const int warp = threadIdx.x / 32, lane = lane_id();
+    const float e = __ldg(a.eps);
+    if (a.score == SC_CAUCHY && blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e)))
+        set_flag(a.ws, FLAG_BAD_EPS);
+    const double ed = (double)e;
+    const int64_t N = a.N;
+    const int k = a.k;
+    for (int u = 0; u < FWD_QPW; ++u) {
+        const int64_t slot = ((int64_t)blockIdx.x * FWD_QPW + u) * FWD_WARPS + warp;
+        if (slot >= a.total) break;
+        const int64_t bh = slot / a.nq;
+        int64_t pos;
+        if (!a.sh.slot_pos(slot - bh * a.nq, N, pos)) continue;
+        const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + bh * N + pos) : pos;
+        const int64_t gq = bh * N + i;
+        float q[DK];
+#pragma unroll
+        for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
+        CandSet<DK> cs;
+        cs.q = q;
+        cs.qc = __ldg(a.qcode + gq);
+        cs.scode = a.scode + bh * N;
+        cs.recs4 = reinterpret_cast<const float4*>(a.recs + bh * N * REC);
+        cs.N = N; cs.M = a.M; cs.W = a.W; cs.causal = a.causal;
+        cs.nruns = a.causal ? i / a.M : 1;
+        const uint64_t qc = cs.qc;
+        const float* recs = a.recs + bh * N * REC;
+        // stream (distance, j, valid) of every candidate, 32 at a time, fixed (run, rank) order
+        auto visit = [&](auto&& f) {
+            for (int64_t c0 = 0; c0 < cs.nruns; c0 += 32) {
+                int64_t base; int w;
+                cs.window(c0 + lane, base, w);
+                const int nc = (int)min64(32, cs.nruns - c0);
+                for (int cc = 0; cc < nc; ++cc) {
+                    const int64_t b = __shfl_sync(FULL, base, cc);
+                    const int ww = __shfl_sync(FULL, w, cc);
+                    for (int r0 = 0; r0 < ww; r0 += 32) {
+                        const bool ok = r0 + lane < ww;
+                        unsigned long long d = ~0ull;
+                        int j = -1;
+                        if (ok) {
+                            const uint64_t kc = __ldg(cs.scode + b + r0 + lane);
+                            d = kc > qc ? kc - qc : qc - kc;
+                            j = __float_as_int(__ldg(recs + (b + r0 + lane) * REC + DK));
+                        }
+                        f(d, j, ok);
+                    }
+                }
+            }
+        };
+        // (1) per-lane L smallest distances -> bound T with #{d <= T} >= k
+        unsigned long long lst[L];
+#pragma unroll
+        for (int t = 0; t < L; ++t) lst[t] = ~0ull;
+        visit([&](unsigned long long d, int, bool ok) {
+            unsigned long long x = ok ? d : ~0ull;
+#pragma unroll
+            for (int t = 0; t < L; ++t) {
+                const unsigned long long lo = umin64(lst[t], x);
+                x = umax64(lst[t], x);
+                lst[t] = lo;
+            }
+        });
+        unsigned long long T;
+        {
+            unsigned finite = 0;
+#pragma unroll
+            for (int t = 0; t < L; ++t) finite += lst[t] != ~0ull;
+            if (__reduce_add_sync(FULL, finite) < (unsigned)k) {
+                T = ~0ull;                                    // fewer than k candidates (or a +inf-like distance)
+            } else {
+                unsigned long long lo = lst[0], hi = 0;
+#pragma unroll
+                for (int t = 0; t < L; ++t) hi = lst[t] != ~0ull ? umax64(hi, lst[t]) : hi;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo = umin64(lo, __shfl_xor_sync(FULL, lo, o));
+                    hi = umax64(hi, __shfl_xor_sync(FULL, hi, o));
+                }
+                while (lo < hi) {                             // smallest T with count(<= T) >= k
+                    const unsigned long long mid = lo + ((hi - lo) >> 1);
+                    unsigned c = 0;
+#pragma unroll
+                    for (int t = 0; t < L; ++t) c += lst[t] <= mid;
+                    if (__reduce_add_sync(FULL, c) >= (unsigned)k) hi = mid; else lo = mid + 1;
+                }
+                T = hi;
+            }
+        }
+        // (2) collect every candidate with d <= T
+        if (lane == 0) s_cnt[warp] = 0;
+        __syncwarp();
+        unsigned long long* sd = s_d[warp];
+        int* sj = s_j[warp];
+        visit([&](unsigned long long d, int j, bool ok) {
+            if (ok && d <= T) {
+                const int p2 = atomicAdd(&s_cnt[warp], 1);
+                if (p2 < CODE_CAP) { sd[p2] = d; sj[p2] = j; }
+            }
+        });
+        __syncwarp();
+        const int cnt = s_cnt[warp];
+        int32_t* idx_row = a.idx + gq * k;
+        if (cnt <= CODE_CAP) {
+            for (int t = lane; t < k; t += 32) idx_row[t] = -1;
+            __syncwarp();
+            for (int m = lane; m < cnt; m += 32) {
+                const unsigned long long dm = sd[m];
+                const int jm = sj[m];
+                int rank = 0;
+                for (int x = 0; x < cnt; ++x) rank += pair_lt(sd[x], sj[x], dm, jm);
+                if (rank < k) idx_row[rank] = jm;
+            }
+        } else {
+            // many equal distances: k rounds of "smallest pair above the last one"
+            unsigned long long ld = 0;
+            int lj = -1;
+            bool first = true;
+            for (int t = 0; t < k; ++t) {
+                unsigned long long bd = ~0ull;
+                int bj = 0x7fffffff;
+                visit([&](unsigned long long d, int j, bool ok) {
+                    if (ok && (first || pair_lt(ld, lj, d, j)) && pair_lt(d, j, bd, bj)) { bd = d; bj = j; }
+                });
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const unsigned long long od = __shfl_xor_sync(FULL, bd, o);
+                    const int oj = __shfl_xor_sync(FULL, bj, o);
+                    if (pair_lt(od, oj, bd, bj)) { bd = od; bj = oj; }
+                }
+                if (lane == 0) idx_row[t] = bj == 0x7fffffff ? -1 : bj;
+                ld = bd; lj = bj; first = false;
+            }
+        }
+        __syncwarp();
+        int jr[R];
+        int nsel = 0;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            Sr[r] = 0.0;
-            if (jr[r] >= 0) {
-                float kj[DK];
-#pragma unroll
-                for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + jr[r]) * DK + d);
-                Sr[r] = score_raw<DK>(sc, q, kj, ed);
-            }
+            const int e2 = r * 32 + lane;
+            jr[r] = e2 < k ? idx_row[e2] : -1;
+            nsel += __popc(__ballot_sync(FULL, jr[r] >= 0));
         }
-        double Smu = 0.0;
-        const int64_t mrow = a.causal ? i : 0;
-        if (a.mean_slot) {
-            float kb[DK];
-#pragma unroll
-            for (int d = 0; d < DK; ++d) kb[d] = __ldg(a.Kbar + (bh * (a.causal ? N : 1) + mrow) * DK + d);
-            Smu = score_raw<DK>(sc, q, kb, ed);
-        }
-        double xmax = 0.0;
-        if (score_is_exp(sc)) {
-            // softmax scores: shift by the largest logit (fixed-order warp max), S = exp(x - xmax)
-            double m = -INFINITY;
-#pragma unroll
-            for (int r = 0; r < R; ++r) m = jr[r] >= 0 ? fmax(m, Sr[r]) : m;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
-            if (a.mean_slot) m = fmax(m, Smu);
-            xmax = m;
-#pragma unroll
-            for (int r = 0; r < R; ++r) Sr[r] = jr[r] >= 0 ? exp(Sr[r] - xmax) : 0.0;
-            if (a.mean_slot) Smu = exp(Smu - xmax);
-        }
-        double zpart = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) zpart += Sr[r];
-        double Zi = warp_sum(zpart);
-        if (a.mean_slot) Zi += Smu;
-        const double invZ = Zi > 0.0 ? 1.0 / Zi : 0.0;
-
-        // ---------------- A7: value gather, float4 chunks, lane groups over slots
-        const int nch = a.dv / 4;
-        int P = 1;
-        while (P < nch && P < 32) P <<= 1;
-        const int G = 32 / P;                 // rows per step (1 when nch >= 32)
-        const int grp = lane / P, ch_l = lane % P;
-        const float* Vb = a.V + bh * N * (int64_t)a.dv;
-        float* orow = a.O + gq * (int64_t)a.dv;
-        const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)a.dv;
-        const double Amu = Smu * invZ;
-        for (int ch0 = 0; ch0 < nch; ch0 += P) {
-            const int ch = ch0 + ch_l;
-            const bool act = ch < nch;
-            double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                if (r * 32 >= nsel) break;
-                for (int t0 = 0; t0 < 32 && r * 32 + t0 < nsel; t0 += 4 * G) {
-                    float4 v4[4];
-                    double A4[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int src = (t0 + u * G + grp) & 31;
-                        const int j = __shfl_sync(FULL, jr[r], src);
-                        A4[u] = __shfl_sync(FULL, Sr[r], src) * invZ;
-                        const bool ok = act && t0 + u * G + grp < 32 && r * 32 + t0 + u * G + grp < nsel;
-                        v4[u] = ok ? __ldg(reinterpret_cast<const float4*>(Vb + (int64_t)j * a.dv) + ch)
-                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (!ok) A4[u] = 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        acc0 = fma(A4[u], (double)v4[u].x, acc0);
-                        acc1 = fma(A4[u], (double)v4[u].y, acc1);
-                        acc2 = fma(A4[u], (double)v4[u].z, acc2);
-                        acc3 = fma(A4[u], (double)v4[u].w, acc3);
-                    }
-                }
-            }
-            for (int o = P; o < 32; o <<= 1) {
-                acc0 += __shfl_xor_sync(FULL, acc0, o);
-                acc1 += __shfl_xor_sync(FULL, acc1, o);
-                acc2 += __shfl_xor_sync(FULL, acc2, o);
-                acc3 += __shfl_xor_sync(FULL, acc3, o);
-            }
-            if (grp == 0 && act) {
-                if (a.mean_slot) {
-                    const float4 vb = __ldg(reinterpret_cast<const float4*>(vbar) + ch);
-                    acc0 = fma(Amu, (double)vb.x, acc0);
-                    acc1 = fma(Amu, (double)vb.y, acc1);
-                    acc2 = fma(Amu, (double)vb.z, acc2);
-                    acc3 = fma(Amu, (double)vb.w, acc3);
-                }
-                reinterpret_cast<float4*>(orow)[ch] =
-                    make_float4((float)acc0, (float)acc1, (float)acc2, (float)acc3);
-            }
-        }
-        if (lane == 0) a.Z[gq] = (float)(score_is_exp(sc) ? (Zi > 0.0 ? xmax + log(Zi) : 0.0) : Zi);
+        attend_row<DK, R>(a, bh, i, gq, q, jr, nsel, ed);
+        __syncwarp();   // s_d/s_j/s_cnt are rewritten by the next query
     }
 }
 
@@ -558,8 +739,12 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
     a.ws = ws;
     const int64_t per_cta = (int64_t)FWD_WARPS * FWD_QPW;
     const unsigned grid = (unsigned)((a.total + per_cta - 1) / per_cta);
-#define ONEDF_FWD_R(RV) \
-    ONEDF_DISPATCH_DK(p->d_k, { if (grid) topk_attn_fwd_kernel<DK, RV><<<grid, FWD_THREADS, 0, st>>>(a); })
+#define ONEDF_FWD_R(RV)                                                                                  \
+    ONEDF_DISPATCH_DK(p->d_k, {                                                                          \
+        if (!grid) {}                                                                                    \
+        else if (p->select) code_select_attn_kernel<DK, RV><<<grid, FWD_THREADS, 0, st>>>(a);           \
+        else topk_attn_fwd_kernel<DK, RV><<<grid, FWD_THREADS, 0, st>>>(a);                             \
+    })
     if (p->k <= 32) { ONEDF_FWD_R(1) }
     else if (p->k <= 64) { ONEDF_FWD_R(2) }
     else if (p->k <= 128) { ONEDF_FWD_R(4) }

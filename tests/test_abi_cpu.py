@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(onedf):
     for name in _declared_functions():
         assert hasattr(lib, name), name
     assert set(onedf.abi.EXPORTS) == set(_declared_functions())
-    assert onedf.onedf_version() == 400
+    assert onedf.onedf_version() == 500
 
 
 def test_struct_layout_matches_c(onedf, tmp_path):
@@ -82,6 +82,8 @@ def test_validate_score_field(onedf):
         assert onedf.onedf_validate(onedf.Problem(*GOOD.values(), 0, 1, score)) == onedf.OK
     for score in (-1, 4):
         assert onedf.onedf_validate(onedf.Problem(*GOOD.values(), 0, 1, score)) == onedf.abi.ERR_INVALID_ARG
+    for sel, want in ((0, "OK"), (1, "OK"), (2, "ERR_INVALID_ARG"), (-1, "ERR_INVALID_ARG")):
+        assert onedf.onedf_validate(onedf.Problem(*GOOD.values(), 0, 1, 0, sel)) == getattr(onedf.abi, want)
 
 
 def test_shard_owner_zigzag(onedf):

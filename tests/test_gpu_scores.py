@@ -92,3 +92,36 @@ def test_score_variant_sequence_sharded(score):
     assert_same(got["idx"], ref["idx"], "idx")
     for n in ("O", "Z", "dQ", "dK", "dV"):
         assert_close(got[n], ref[n], n)
+
+
+# ---------------------------------------------------------------- selection variant: SPEC's code-distance merge (D25)
+SEL_CASES = {
+    "spec_w_eq_k": dict(B=1, H=2, N=1024, d_k=3, d_v=16, k=16, window=16, chunk=128, causal=1, mean_slot=1),
+    "wide_window": dict(B=2, H=1, N=600, d_k=2, d_v=8, k=8, window=40, chunk=64, causal=1, mean_slot=1),
+    "noncausal": dict(B=1, H=2, N=300, d_k=3, d_v=8, k=12, window=24, chunk=1, causal=0, mean_slot=0),
+    "k64_many_runs": dict(B=1, H=1, N=4096, d_k=3, d_v=64, k=64, window=64, chunk=128, causal=1, mean_slot=1),
+    "dk1": dict(B=1, H=1, N=512, d_k=1, d_v=8, k=8, window=8, chunk=32, causal=1, mean_slot=1),
+}
+
+
+@pytest.mark.parametrize("name", list(SEL_CASES))
+def test_code_distance_selection_parity(name):
+    kw = dict(SEL_CASES[name], select=1)
+    x = _inputs(kw, seed=zlib.crc32(name.encode()) % 1000)
+    got, ref = gpu_run(kw, x), oracle_run(kw, x)
+    assert_same(got["idx"], ref["idx"], "idx")
+    for n in ("O", "Z", "dQ", "dK", "dV", "d_eps"):
+        assert_close(got[n], ref[n], n)
+
+
+@pytest.mark.parametrize("score", [0, 1])
+def test_code_distance_selection_repeated_codes(score):
+    """Repeated codes (3 bits per dim, few distinct rows) put many candidates at the same code
+    distance: the fallback ordering must still give the oracle's (distance, j) order."""
+    kw = dict(B=1, H=2, N=512, d_k=3, d_v=16, k=16, window=48, chunk=64, bits=3, causal=1, mean_slot=1,
+              score=score, select=1)
+    x = _inputs(kw, seed=17, dup_keys=True)
+    got, ref = gpu_run(kw, x), oracle_run(kw, x)
+    assert_same(got["idx"], ref["idx"], "idx")
+    for n in ("O", "dQ", "dK", "dV"):
+        assert_close(got[n], ref[n], n)
