@@ -119,6 +119,19 @@ __device__ __forceinline__ void merge_pending(unsigned long long (&top)[R], unsi
     }
 }
 
+// The first 32*RS of buf[0..cnt) (KEY_MAX-padded), bitonic-sorted into top[0..RS); top[RS..R) = KEY_MAX.
+template <int RS, int R>
+__device__ __forceinline__ void sort_rows(const unsigned long long* buf, int cnt, unsigned long long (&top)[R]) {
+    const int lane = lane_id();
+    unsigned long long x[RS];
+#pragma unroll
+    for (int r = 0; r < RS; ++r) x[r] = r * 32 + lane < cnt ? buf[r * 32 + lane] : KEY_MAX;
+    if (RS == 1) x[0] = warp_sort32(x[0]);
+    else warp_sort<RS>(x);
+#pragma unroll
+    for (int r = 0; r < R; ++r) top[r] = r < RS ? x[r < RS ? r : 0] : KEY_MAX;
+}
+
 // Element e of the distributed list (e runtime, warp-uniform).
 template <int R>
 __device__ __forceinline__ unsigned long long list_get(const unsigned long long (&top)[R], int e) {
@@ -483,11 +496,16 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         __syncwarp();
         unsigned long long top[R];
         if (fits) {
-            // ---------------- exact order of the collected keys: 32-key rows merged into the
-            // register top list (shuffle bitonic sort of the row + min-merge + half-cleaners)
-#pragma unroll
-            for (int r = 0; r < R; ++r) top[r] = KEY_MAX;
-            for (int m = 0; m * 32 < cnt; ++m)
+            // ---------------- exact order of the collected keys: the first rows (up to R) are
+            // bitonic-sorted together into the register top list, every further 32-key row is
+            // merged in (shuffle bitonic sort of the row + min-merge + half-cleaners)
+            const int rows = (cnt + 31) / 32;
+            int m0;
+            if (rows <= 1 || R == 1) { sort_rows<1, R>(buf, cnt, top); m0 = 1; }
+            else if (rows <= 2 || R == 2) { sort_rows<(R >= 2 ? 2 : 1), R>(buf, cnt, top); m0 = 2; }
+            else if (rows <= 4 || R == 4) { sort_rows<(R >= 4 ? 4 : 1), R>(buf, cnt, top); m0 = 4; }
+            else { sort_rows<(R >= 8 ? 8 : 1), R>(buf, cnt, top); m0 = 8; }
+            for (int m = m0; m * 32 < cnt; ++m)
                 merge_pending<R>(top, m * 32 + lane < cnt ? buf[m * 32 + lane] : KEY_MAX);
         } else {
             // ---------------- rare: too many keys at or below T (e.g. many equal
