@@ -50,9 +50,6 @@ constexpr int FWD_THREADS = FWD_WARPS * 32;
 #ifndef ONEDF_FWD_MINB
 #define ONEDF_FWD_MINB 4
 #endif
-#ifndef ONEDF_FWD_COLLECT
-#define ONEDF_FWD_COLLECT 1          // pass-2 append: 0 ballot + popc compaction, 1 shared-memory atomic cursor
-#endif
 constexpr int FWD_QPW = ONEDF_FWD_QPW;              // queries per warp (schedule stretch per CTA = 8*QPW)
 constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 loaded ahead (W = 128 -> one window)
 constexpr int FWD_CAP = 256;                        // pass-2 collection capacity per warp
@@ -368,7 +365,7 @@ __device__ __forceinline__ void attend_row(const FwdArgs& a, int64_t bh, int64_t
 template <int DK, int R>
 __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_kernel(const FwdArgs a) {
     constexpr int L = PassOne<R>::L;
-    __shared__ __align__(16) unsigned long long s_buf[FWD_WARPS][FWD_CAP + 32 * FWD_UB];
+    __shared__ __align__(16) unsigned long long s_buf[FWD_WARPS][FWD_CAP];
     __shared__ int s_cnt[FWD_WARPS];
     const int warp = threadIdx.x / 32, lane = lane_id();
     unsigned long long* buf = s_buf[warp];
@@ -455,7 +452,6 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         // ---------------- A6 pass 2: collect every candidate with D <= T (order is
         // irrelevant: the final order comes from ranking the unique keys)
         int cnt = 0;
-#if ONEDF_FWD_COLLECT == 1
         if (lane == 0) s_cnt[warp] = 0;
         __syncwarp();
         cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB], const bool (&ok)[FWD_UB], int,
@@ -472,19 +468,6 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         __syncwarp();
         cnt = s_cnt[warp];
         const bool fits = cnt <= FWD_CAP;
-#else
-        const bool fits = cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB],
-                                                  const bool (&ok)[FWD_UB], int, int) {
-#pragma unroll
-            for (int uu = 0; uu < FWD_UB; ++uu) {
-                const bool pass = ok[uu] && __float_as_uint(D[uu]) <= tb;
-                const unsigned m = __ballot_sync(FULL, pass);
-                if (pass) buf[cnt + __popc(m & lanemask_lt())] = make_key(D[uu], jj[uu]);
-                cnt += __popc(m);
-            }
-            return cnt <= FWD_CAP;                     // buf has FWD_CAP + 32*FWD_UB slots
-        });
-#endif
 #ifdef ONEDF_FWD_STATS
         if (lane == 0) {
             atomicAdd(&g_fwd_stats[0], 1ull);
