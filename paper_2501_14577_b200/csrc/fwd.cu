@@ -52,6 +52,9 @@ constexpr int FWD_THREADS = FWD_WARPS * 32;
 #endif
 constexpr int FWD_QPW = ONEDF_FWD_QPW;              // queries per warp (schedule stretch per CTA = 8*QPW)
 constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 loaded ahead (W = 128 -> one window)
+#ifndef ONEDF_FWD_TBITS
+#define ONEDF_FWD_TBITS 18                          // bisection of T stops at 2^(TBITS-23) relative width
+#endif
 constexpr int FWD_CAP = 256;                        // pass-2 collection capacity per warp
 constexpr unsigned long long KEY_MAX = ~0ull;
 
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         });
         // T: a bit pattern with #{values <= T} >= k (non-negative floats order as
         // their bits).  Bisection between the smallest list head and the largest
-        // list tail, stopped at ~2^-8 relative resolution: any such T is a valid
+        // list tail, stopped at 2^(TBITS-23) relative width: any such T is a valid
         // bound, a slightly larger one only admits a few more keys in pass 2.
         unsigned tb;
         {
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
             } else {
                 unsigned lo = __float_as_uint(fmn), hi = __float_as_uint(fmx);   // count(<= hi) >= k
 #pragma unroll 1
-                while (hi - lo > (1u << 15)) {          // 2^-8 of a mantissa step
+                while (hi - lo > (1u << ONEDF_FWD_TBITS)) {   // stop at 2^(TBITS-23) relative resolution
                     const unsigned mid = lo + ((hi - lo) >> 1);
                     unsigned c = 0;
 #pragma unroll
