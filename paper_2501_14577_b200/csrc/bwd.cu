@@ -112,7 +112,7 @@ __device__ __forceinline__ void slot_w(int sc, const float* q, const float* kj, 
     }
 }
 
-template <int DK, int P, int CH, int R>
+template <int DK, int P, int CH, int R, bool WHOLE>
 __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(const BwdArgs a) {
     constexpr int G = 32 / P;                    // rows per step
     constexpr int T = P < 8 ? P : 8;             // steps per block (live partials / loads in flight per lane)
@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
     }
     const int64_t mrow = a.causal ? i : 0;
     const float* Vb = a.V + bh * N * (int64_t)dv;
+    const float4* V4 = reinterpret_cast<const float4*>(Vb);
     const int owner_t = l >> (LOGP - LOGT);
     const bool owner = (l & ((1 << (LOGP - LOGT)) - 1)) == 0;
     double* sp = s_part[warp];
@@ -173,11 +174,12 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 const int j = __shfl_sync(FULL, jr[r], (h0 + t * G + grp) & 31);
-                const float4* vr = reinterpret_cast<const float4*>(Vb + (int64_t)(j < 0 ? 0 : j) * dv);
+                // an unselected slot (j < 0) reads row 0; its dot is never used (phase 2 skips it)
+                const float4* vr = V4 + (int64_t)(j < 0 ? 0 : j) * nch + l;
 #pragma unroll
                 for (int h = 0; h < CH; ++h) {
-                    const int ch = l + h * P;
-                    x[t][h] = (j >= 0 && ch < nch) ? __ldg(vr + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (WHOLE) x[t][h] = __ldg(vr + h * P);            // P*CH == d_v/4: every chunk exists
+                    else x[t][h] = l + h * P < nch ? __ldg(vr + h * P) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
 #pragma unroll
@@ -547,16 +549,20 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
         if (e != cudaSuccess) return e;
     }
     const int P = lanes_per_row(p->d_v);
+    const int nch = p->d_v / 4;
     const unsigned qgrid = (unsigned)((a.total + BWD_WARPS - 1) / BWD_WARPS);
     const unsigned kgrid = (unsigned)((total + BWD_WARPS - 1) / BWD_WARPS);
+#define ONEDF_BWDQW(PV, CHV, RV)                                                                        \
+    if (PV * CHV == nch) bwd_query_kernel<DK, PV, CHV, RV, true><<<qgrid, BWD_THREADS, 0, st>>>(a);      \
+    else bwd_query_kernel<DK, PV, CHV, RV, false><<<qgrid, BWD_THREADS, 0, st>>>(a);
 #define ONEDF_BWDQR(PV, RV)                                                                            \
     ONEDF_DISPATCH_DK(p->d_k, {                                                                        \
         if constexpr (PV == 32) {                                                                      \
             if (!qgrid) {}                                                                            \
-            else if (p->d_v > 128) bwd_query_kernel<DK, PV, 2, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);  \
-            else bwd_query_kernel<DK, PV, 1, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);                    \
+            else if (p->d_v > 128) { ONEDF_BWDQW(PV, 2, RV) }                                          \
+            else { ONEDF_BWDQW(PV, 1, RV) }                                                            \
         } else if (qgrid) {                                                                            \
-            bwd_query_kernel<DK, PV, 1, RV><<<qgrid, BWD_THREADS, 0, st>>>(a);                         \
+            ONEDF_BWDQW(PV, 1, RV)                                                                     \
         }                                                                                              \
     })
 #define ONEDF_BWDQ(PV)                      \
@@ -570,6 +576,7 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     else { ONEDF_BWDQ(32) }
 #undef ONEDF_BWDQ
 #undef ONEDF_BWDQR
+#undef ONEDF_BWDQW
     tr.mark(2, st);
     KeyArgs ka;
     ka.Q = Q; ka.K = K; ka.dO = dO; ka.offsets = t->offsets; ka.rec = t->rec;
