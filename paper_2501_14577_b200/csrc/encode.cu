@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_kernel(
     const float* __restrict__ Q, const float* __restrict__ K, int64_t N, int b, bool vec_ok,
     const float* __restrict__ part, int splits, const double* __restrict__ lohi_in,
     uint64_t* __restrict__ qcode, uint64_t* __restrict__ kcode, double* __restrict__ lohi_out,
-    void* ws) {
+    void* ws, Shard sh) {
     const int64_t bh = blockIdx.y;
     __shared__ double s_lo[DK], s_hi[DK];
     if (threadIdx.x < DK) {
@@ -185,6 +185,13 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_kernel(
     const double top = (double)((1ull << b) - 1ull);
     const int64_t g = (int64_t)blockIdx.x * ENC_THREADS + threadIdx.x;
     if (g * ENC_ROWS >= N) return;
+    // sharded: codes of other ranks' rows are never read (their runs arrive by all-gather)
+    if (sh.on()) {
+        bool any = false;
+#pragma unroll
+        for (int r = 0; r < ENC_ROWS; ++r) any |= g * ENC_ROWS + r < N && sh.owns_row(g * ENC_ROWS + r);
+        if (!any) return;
+    }
     const int64_t row0 = bh * N + g * ENC_ROWS;
     const int64_t nrows = min64(ENC_ROWS, N - g * ENC_ROWS);
 #pragma unroll
@@ -232,7 +239,7 @@ cudaError_t launch_encode(const onedf_problem* p, int b, const float* Q, const f
         bounds_partial_kernel<DK><<<dim3(splits, (unsigned)BH), ENC_THREADS, 0, st>>>(Q, K, N, splits, vec_ok, part,
                                                                                       ws, make_shard(p));
         encode_kernel<DK><<<egrid, ENC_THREADS, 0, st>>>(Q, K, N, b, vec_ok, part, splits, lohi_in, qcode, kcode,
-                                                         lohi_out, ws);
+                                                         lohi_out, ws, make_shard(p));
     });
     return cudaGetLastError();
 }

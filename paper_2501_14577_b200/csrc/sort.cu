@@ -29,11 +29,12 @@ constexpr int SEG_BIG_WARPS = 32;      // runs longer than SEG_SORT_MAX: keys st
 template <bool SMEM>
 __global__ void __launch_bounds__((SMEM ? SEG_MAX_WARPS : SEG_BIG_WARPS) * 32) seg_sort_kernel(
     const uint64_t* __restrict__ kcode, uint64_t* __restrict__ scode, int32_t* __restrict__ perm,
-    int64_t N, int64_t M, int64_t runs_per_bh, SortScratch scr) {
+    int64_t N, int64_t M, int64_t runs_per_bh, SortScratch scr, Shard sh) {
     using Pos = typename std::conditional<SMEM, uint16_t, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem[];
     const int64_t bh = blockIdx.x / runs_per_bh;
     const int64_t c = blockIdx.x % runs_per_bh;
+    if (sh.on() && Shard::owner(c, sh.world) != sh.rank) return;   // sharded: other ranks' runs arrive by all-gather
     const int64_t s0 = c * M;
     const int n = (int)min64(M, N - s0);
     const int nw = blockDim.x / 32;
@@ -169,7 +170,7 @@ cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint6
     if (M > SEG_SORT_MAX) {
         const size_t smem = 256 * (size_t)SEG_BIG_WARPS * 4;
         seg_sort_kernel<false><<<(unsigned)(BH * runs), SEG_BIG_WARPS * 32, smem, st>>>(kcode, scode, perm, N, M,
-                                                                                        runs, scr);
+                                                                                        runs, scr, make_shard(p));
         return cudaGetLastError();
     }
     int nw = (int)((M + 32 * 8 - 1) / (32 * 8));   // ~8 keys per lane
@@ -177,7 +178,8 @@ cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint6
     const size_t smem = seg_sort_smem(M, nw);
     cudaError_t e = cudaFuncSetAttribute(seg_sort_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    seg_sort_kernel<true><<<(unsigned)(BH * runs), nw * 32, smem, st>>>(kcode, scode, perm, N, M, runs, scr);
+    seg_sort_kernel<true><<<(unsigned)(BH * runs), nw * 32, smem, st>>>(kcode, scode, perm, N, M, runs, scr,
+                                                                       make_shard(p));
     return cudaGetLastError();
 }
 

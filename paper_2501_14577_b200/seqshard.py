@@ -125,12 +125,31 @@ def _rank_order_sum(xs):
 
 
 # ---------------------------------------------------------------- single-process driver (one GPU, all ranks)
-def run_sim(gens, plan: ShardPlan):
-    """Drive `world` step() generators in lock step; the collectives are copies."""
+def run_sim(gens, plan: ShardPlan, timing: list | None = None):
+    """Drive `world` step() generators in lock step; the collectives are copies.
+
+    timing: if a list is given, it receives each rank's device time (ms) spent in its own
+    segments between collectives (CUDA events around every segment; the simulated
+    collectives are excluded) -- the per-rank compute of a real sharded run."""
     world = len(gens)
     results = [None] * world
     done = [False] * world
-    reqs = [next(g) for g in gens]
+    segs = [[] for _ in range(world)]
+
+    def advance(r, value, first=False):
+        e0 = e1 = None
+        if timing is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        try:
+            out = next(gens[r]) if first else gens[r].send(value)
+        finally:
+            if timing is not None:
+                e1.record()
+                segs[r].append((e0, e1))
+        return out
+
+    reqs = [advance(r, None, first=True) for r in range(world)]
     while not all(done):
         kind = reqs[0][0]
         assert all(r[0] == kind for r in reqs), "ranks diverged"
@@ -162,11 +181,27 @@ def run_sim(gens, plan: ShardPlan):
             raise ValueError(kind)
         for r in range(world):
             try:
-                reqs[r] = gens[r].send(replies[r])
+                reqs[r] = advance(r, replies[r])
             except StopIteration as e:
                 results[r] = e.value
                 done[r] = True
+    if timing is not None:
+        torch.cuda.synchronize()
+        timing.extend(sum(a.elapsed_time(b) for a, b in segs[r]) for r in range(world))
     return results
+
+
+def exchange_bytes(p: abi.Problem, plan: ShardPlan, backward: bool = True) -> dict:
+    """Bytes one rank sends per step in run_dist (payloads as packed): the bounds all-reduce,
+    the all-gather of its rows of scode (8 B), perm (4 B), K (4 d_k B) and V (4 d_v B) to the
+    other ranks, and (backward) the all-to-all of its partial dK, dV rows owned by others
+    plus the d_eps all-gather."""
+    P, BH, rows = plan.world, p.B * p.H, plan.rows_max
+    bounds = 2 * 2 * p.d_k * 8 * BH * max(P - 1, 0)
+    gather = (P - 1) * BH * rows * (8 + 4 + 4 * p.d_k + 4 * p.d_v)
+    reduce = (P - 1) * BH * rows * 4 * (p.d_k + p.d_v) if backward else 0
+    return {"bounds": bounds, "gather_runs_rows": gather, "reduce_partials": reduce,
+            "total": bounds + gather + reduce + (8 * (P - 1) if backward else 0)}
 
 
 # ---------------------------------------------------------------- one process per rank (torch.distributed)

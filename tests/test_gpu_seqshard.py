@@ -149,3 +149,13 @@ def test_rank_sum_is_rank_ordered_f64():
     for q in parts[1:]:
         acc = acc + q.double()
     assert torch.equal(got, acc.float())
+
+
+def test_seq_sharded_tiny_chunks():
+    """Chunks shorter than the encoder's 4-row groups (M = 3): ownership changes inside a group."""
+    world, kw = 3, dict(B=1, H=1, N=200, d_k=3, d_v=8, k=4, window=8, chunk=3, causal=1, mean_slot=1)
+    x = _inputs(kw, seed=21)
+    got, ref = sharded_run(kw, x, world), oracle_run(kw, x)
+    assert_same(got["idx"], ref["idx"], "idx")
+    for n in ("O", "dQ", "dK", "dV"):
+        assert_close(got[n], ref[n], n)
