@@ -351,6 +351,14 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
     const int4* rec = a.rec + bh * a.L + s0;
     const int dv = a.dv, nch = dv / 4;
     const int grp = lane / P, l = lane % P;
+    if (len == 0) {
+        // no query selected this key (e.g. the last chunk's keys, or another rank's queries):
+        // its direct gradient is zero (the mean-slot scan adds its share afterwards)
+        float4* dvrow = reinterpret_cast<float4*>(a.dV + gk * (int64_t)dv);
+        for (int ch = lane; ch < nch; ch += 32) dvrow[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane < DK) a.dK[gk * DK + lane] = 0.f;
+        return;
+    }
 
     // ---- fixed visiting order: ascending query position i (distinct within a segment)
     const bool small = len <= KEY_REG_SEG && N < (1ll << (32 - KEY_POS_BITS));
