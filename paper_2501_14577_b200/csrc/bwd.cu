@@ -1,6 +1,6 @@
 // bwd.cu -- A8 backward query side (K7), A10 key side (K9), A12 eps reduce
-// (K11).  The transpose (A9, K8) is in sort.cu and the mean-slot chain rule
-// (A11, K10) in mean.cu.
+// (K11).  The transpose (A9, K8: in-degree count + CSR offsets) is in csr.cu
+// and the mean-slot chain rule (A11, K10) in mean.cu.
 //
 // Appendix, with "dL/do_i . (v_j - o_i)/Z_i" read as a d_v-wide
 // dot product (D15) and I held fixed (D16):
@@ -10,23 +10,27 @@
 //   deps  = -sum_ij g_ij / delta^2
 //   dv_j  = sum_{i: j in I_i} A_ij dO_i
 //   dk_j  = sum_{i: j in I_i} w_ij (q_i - k_j)
-// plus the mean slot as one more slot (its A, w go to the A11 scan).
+// plus the mean slot as one more slot (its A, w go to the A11 scan), and the
+// score variants' weights and w (D24, slot_w).
 //
 // K7: one warp per query, queries visited in the Morton schedule (optional;
 // see fwd.cu) so neighbouring warps gather overlapping V rows through L1.
-// P lanes read one v_j row (P float4 chunks = one coalesced 256-B row at
-// d_v = 64), each lane dots its chunk with its slice of dO_i (f64, exact f32
-// products); after T steps every lane holds T partial dots of T different
-// rows, and a butterfly reduce-scatter (log2 P xor-shuffle levels, halving
-// the live values each level) leaves each row's full dot product on one
-// lane.  That lane forms g, A, w for its slot, writes the (A, w) pair the
-// key side consumes, and accumulates dq and deps in f64.
+// Phase 1: P lanes read one v_j row (P float4 chunks = one coalesced 256-B row
+// at d_v = 64), each lane dots its chunk with its slice of dO_i (f64, exact
+// f32 products); after T steps every lane holds T partial dots of T rows and a
+// butterfly reduce-scatter (log2 P xor-shuffle levels, halving the live values
+// each level) leaves each row's dot on one lane, which parks it in shared
+// memory.  Phase 2, lane-parallel over the slots: Z_i and c_i = sum_j A_ij
+// (dO_i.v_j) + A_imu dO_i.Vbar_i recomputed in f64 (reading R3), then g, A, w
+// per slot, dq and deps in f64, and each (i, A, w) record appended to its
+// key's CSR segment (integer cursor, csr.cu).
 // K9: one warp per key j (keys visited in sorted-run order when perm is
-// given) walks its CSR segment of (query, slot) pairs in ascending slot order
-// (fixed by the stable transpose): lanes load 32 entries at a time
-// (coalesced), lane groups of P gather the dO_i rows, f64 accumulators, a
-// fixed shuffle tree at the end -- a deterministic segment reduction, no
-// float atomics.  Every per-row result is independent of the visiting order.
+// given) orders its CSR segment by query position (register bitonic sort of
+// (i << 8 | position) keys up to 256 entries, rank counting beyond), then
+// walks it 32 entries at a time: lane groups of P gather the dO_i rows into
+// f64 accumulators, a fixed shuffle tree at the end -- a deterministic
+// segment reduction, no float atomics.  Every per-row result is independent
+// of the visiting order and of the atomic interleaving.
 #include "common.cuh"
 #include "internal.h"
 
