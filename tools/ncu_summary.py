@@ -35,7 +35,7 @@ METRICS = [
 STALL = "smsp__average_warps_issue_stalled_"
 # kernel name -> bench phase key (ncu_traffic.json)
 PHASE = {"topk_attn_fwd_kernel": "fwd_topk", "bwd_query_kernel": "bwd_query", "bwd_key_kernel": "bwd_key",
-         "tr_downsweep_kernel": "bwd_transpose_downsweep"}
+         "csr_count_kernel": "bwd_csr_count"}
 
 
 def raw(rep):
