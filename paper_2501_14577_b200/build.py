@@ -18,7 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
          "--fmad=true", "-I", INCLUDE, "-I", CSRC]
-SOURCES = ["encode.cu", "sort.cu", "mean.cu", "fwd.cu", "bwd.cu", "csr.cu", "workload.cu", "abi.cu"]
+SOURCES = ["encode.cu", "sort.cu", "mean.cu", "fwd.cu", "bwd.cu", "bwd_dk12.cu", "bwd_dk34.cu", "bwd_dk56.cu",
+           "bwd_dk78.cu", "csr.cu", "workload.cu", "abi.cu"]
 
 
 def _stale(out: str, deps) -> bool:
