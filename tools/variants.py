@@ -2,6 +2,7 @@
 
     python tools/variants.py [--src fwd.cu,bwd.cu] NAME=DEF1,DEF2 ...
         e.g.  python tools/variants.py --src fwd.cu ub2_b3=ONEDF_FWD_UB=2,ONEDF_FWD_MINB=3
+              (backward kernel macros: --src bwd_dk12.cu,bwd_dk34.cu,bwd_dk56.cu,bwd_dk78.cu)
 Each lands in build_variants/NAME/libonedf.so; select one with ONEDF_LIB=... (tools only).
 With --src only those sources are recompiled with the defines; the other objects are
 copied from the product build (paper_2501_14577_b200/build/), which must be current.
