@@ -422,20 +422,25 @@ int oref_forward(const oref_problem* p, const float* Q, const float* K, const fl
     const int dk = p->d_k, dv = p->d_v, k = p->k;
     if (!(eps > 0.0) || !isfinite(eps)) return OREF_ERR_NONFINITE;
     if (!sel) {
-        #pragma omp parallel for schedule(dynamic)
+        /* queries are independent given the prefix means: OpenMP over the
+         * queries of each (b,h) (every output row is computed by the same
+         * serial code whichever thread runs it) */
+        double* Kb = NULL; double* Vb = NULL;
+        if (p->mean_slot) {
+            Kb = (double*)malloc(sizeof(double) * (size_t)(N * dk));
+            Vb = (double*)malloc(sizeof(double) * (size_t)(N * dv));
+        }
         for (int64_t bh = 0; bh < BH; ++bh) {
-            double* Kb = NULL; double* Vb = NULL;
             if (p->mean_slot) {
-                Kb = (double*)malloc(sizeof(double) * (size_t)(N * dk));
-                Vb = (double*)malloc(sizeof(double) * (size_t)(N * dv));
                 prefix_means(p, K, bh, dk, Kb);
                 prefix_means(p, V, bh, dv, Vb);
             }
+            #pragma omp parallel for schedule(dynamic, 64)
             for (int64_t i = 0; i < N; ++i)
                 forward_query(p, bh, i, Q, K, V, eps, idx + (bh * N + i) * k, Kb, Vb,
                               O + (bh * N + i) * dv, Z + bh * N + i);
-            free(Kb); free(Vb);
         }
+        free(Kb); free(Vb);
         return OREF_OK;
     }
     double* Kb = NULL; double* Vb = NULL; int64_t cur_bh = -1;
@@ -466,82 +471,148 @@ int oref_forward(const oref_problem* p, const float* Q, const float* K, const fl
  *   deps  = -sum_i sum_j g_ij/delta^2
  * plus the mean slot as one more slot whose key/value are prefix means, its
  * gradients chained back with weight 1/(i+1) (causal) or 1/N (D8, S:323(a)).
- * Accumulation order: queries ascending, slots ascending, mean slot last.   */
+ * Accumulation order: queries ascending, slots ascending, mean slot last.
+ * Per (b,h), in two loops so the host cores can share the work without
+ * changing any sum's order:
+ *   (1) per query (OpenMP over i; each query writes only its own rows):
+ *       Z_i, o_i, g_ij and delta_ij of every slot, dq_i, the mean slot's
+ *       dKbar_i/dVbar_i;
+ *   (2) the key-side sums dv_j, dk_j (OpenMP over disjoint key ranges, each
+ *       thread walking ALL (i, slot) pairs in ascending order and applying
+ *       those of its own keys -- every key's sum runs in ascending i), and
+ *       deps over (i, slot) in ascending order (serial).                   */
 int oref_backward(const oref_problem* p, const float* Q, const float* K, const float* V, double eps,
                   const int32_t* idx, const float* dO, double* dQ, double* dK, double* dV, double* d_eps) {
     const int64_t BH = p->B * p->H, N = p->N;
     const int dk = p->d_k, dv = p->d_v, k = p->k;
     if (!(eps > 0.0) || !isfinite(eps)) return OREF_ERR_NONFINITE;
-    double* eps_part = (double*)calloc((size_t)BH, sizeof(double));
-    #pragma omp parallel for schedule(dynamic)
+    double* Kb = NULL; double* Vb = NULL; double* dKb = NULL; double* dVb = NULL;
+    if (p->mean_slot) {
+        Kb = (double*)malloc(sizeof(double) * (size_t)(N * dk));
+        Vb = (double*)malloc(sizeof(double) * (size_t)(N * dv));
+        dKb = (double*)malloc(sizeof(double) * (size_t)(N * dk));
+        dVb = (double*)malloc(sizeof(double) * (size_t)(N * dv));
+    }
+    /* per (query, slot) g and delta (slot k = the mean slot), per query Z and "attended" */
+    double* gs = (double*)malloc(sizeof(double) * (size_t)(N * (k + 1)));
+    double* ds = (double*)malloc(sizeof(double) * (size_t)(N * (k + 1)));
+    double* Zs = (double*)malloc(sizeof(double) * (size_t)N);
+    double deps = 0.0;
     for (int64_t bh = 0; bh < BH; ++bh) {
-        double* Kb = NULL; double* Vb = NULL; double* dKb = NULL; double* dVb = NULL;
+        double deps_bh = 0.0;
         if (p->mean_slot) {
-            Kb = (double*)malloc(sizeof(double) * (size_t)(N * dk));
-            Vb = (double*)malloc(sizeof(double) * (size_t)(N * dv));
-            dKb = (double*)calloc((size_t)(N * dk), sizeof(double));
-            dVb = (double*)calloc((size_t)(N * dv), sizeof(double));
             prefix_means(p, K, bh, dk, Kb);
             prefix_means(p, V, bh, dv, Vb);
+            for (int64_t x = 0; x < N * dk; ++x) dKb[x] = 0.0;
+            for (int64_t x = 0; x < N * dv; ++x) dVb[x] = 0.0;
         }
-        double* o = (double*)malloc(sizeof(double) * (size_t)dv);
         for (int64_t x = 0; x < N * dk; ++x) { dQ[bh * N * dk + x] = 0.0; dK[bh * N * dk + x] = 0.0; }
         for (int64_t x = 0; x < N * dv; ++x) dV[bh * N * dv + x] = 0.0;
-        double deps = 0.0;
-        for (int64_t i = 0; i < N; ++i) {
-            const int64_t fi = bh * N + i;
-            const float* q = Q + fi * dk;
-            const float* g_o = dO + fi * dv;
-            const int32_t* row = idx + fi * k;
-            /* forward quantities for this query */
-            double Zi = 0.0, Smu = 0.0;
-            for (int r = 0; r < k; ++r)
-                if (row[r] >= 0) Zi += 1.0 / (dist64(q, K + (bh * N + row[r]) * dk, dk) + eps);
-            if (p->mean_slot) { Smu = 1.0 / (dist64_mean(q, Kb + i * dk, dk) + eps); Zi += Smu; }
-            if (!(Zi > 0.0)) continue;                      /* D7: nothing attended */
-            for (int d = 0; d < dv; ++d) o[d] = 0.0;
-            for (int r = 0; r < k; ++r) {
-                if (row[r] < 0) continue;
-                int64_t j = row[r];
-                double A = (1.0 / (dist64(q, K + (bh * N + j) * dk, dk) + eps)) / Zi;
-                for (int d = 0; d < dv; ++d) o[d] += A * (double)V[(bh * N + j) * dv + d];
-            }
-            if (p->mean_slot)
-                for (int d = 0; d < dv; ++d) o[d] += (Smu / Zi) * Vb[i * dv + d];
-            /* gradients */
-            for (int r = 0; r < k; ++r) {
-                if (row[r] < 0) continue;
-                int64_t j = row[r];
-                const float* kj = K + (bh * N + j) * dk;
-                double delta = dist64(q, kj, dk) + eps;
-                double A = (1.0 / delta) / Zi;
-                double dot = 0.0;
-                for (int d = 0; d < dv; ++d) dot += (double)g_o[d] * ((double)V[(bh * N + j) * dv + d] - o[d]);
-                double g = dot / Zi;
-                for (int d = 0; d < dv; ++d) dV[(bh * N + j) * dv + d] += A * (double)g_o[d];
-                for (int d = 0; d < dk; ++d) {
-                    double diff = (double)q[d] - (double)kj[d];
-                    dQ[fi * dk + d] += -2.0 * g * diff / (delta * delta);
-                    dK[(bh * N + j) * dk + d] += 2.0 * g * diff / (delta * delta);
+        /* (1) per query */
+        #pragma omp parallel
+        {
+            double* o = (double*)malloc(sizeof(double) * (size_t)dv);
+            #pragma omp for schedule(dynamic, 64)
+            for (int64_t i = 0; i < N; ++i) {
+                const int64_t fi = bh * N + i;
+                const float* q = Q + fi * dk;
+                const float* g_o = dO + fi * dv;
+                const int32_t* row = idx + fi * k;
+                /* forward quantities for this query */
+                double Zi = 0.0, Smu = 0.0;
+                for (int r = 0; r < k; ++r)
+                    if (row[r] >= 0) Zi += 1.0 / (dist64(q, K + (bh * N + row[r]) * dk, dk) + eps);
+                if (p->mean_slot) { Smu = 1.0 / (dist64_mean(q, Kb + i * dk, dk) + eps); Zi += Smu; }
+                Zs[i] = Zi;
+                if (!(Zi > 0.0)) continue;                      /* D7: nothing attended */
+                for (int d = 0; d < dv; ++d) o[d] = 0.0;
+                for (int r = 0; r < k; ++r) {
+                    if (row[r] < 0) continue;
+                    int64_t j = row[r];
+                    double A = (1.0 / (dist64(q, K + (bh * N + j) * dk, dk) + eps)) / Zi;
+                    for (int d = 0; d < dv; ++d) o[d] += A * (double)V[(bh * N + j) * dv + d];
                 }
-                deps += -g / (delta * delta);
-            }
-            if (p->mean_slot) {
-                const double* kb = Kb + i * dk;
-                double delta = dist64_mean(q, kb, dk) + eps;
-                double A = Smu / Zi;
-                double dot = 0.0;
-                for (int d = 0; d < dv; ++d) dot += (double)g_o[d] * (Vb[i * dv + d] - o[d]);
-                double g = dot / Zi;
-                for (int d = 0; d < dv; ++d) dVb[i * dv + d] += A * (double)g_o[d];
-                for (int d = 0; d < dk; ++d) {
-                    double diff = (double)q[d] - kb[d];
-                    dQ[fi * dk + d] += -2.0 * g * diff / (delta * delta);
-                    dKb[i * dk + d] += 2.0 * g * diff / (delta * delta);
+                if (p->mean_slot)
+                    for (int d = 0; d < dv; ++d) o[d] += (Smu / Zi) * Vb[i * dv + d];
+                /* gradients of the query side */
+                for (int r = 0; r < k; ++r) {
+                    if (row[r] < 0) continue;
+                    int64_t j = row[r];
+                    const float* kj = K + (bh * N + j) * dk;
+                    double delta = dist64(q, kj, dk) + eps;
+                    double dot = 0.0;
+                    for (int d = 0; d < dv; ++d) dot += (double)g_o[d] * ((double)V[(bh * N + j) * dv + d] - o[d]);
+                    double g = dot / Zi;
+                    gs[i * (k + 1) + r] = g;
+                    ds[i * (k + 1) + r] = delta;
+                    for (int d = 0; d < dk; ++d) {
+                        double diff = (double)q[d] - (double)kj[d];
+                        dQ[fi * dk + d] += -2.0 * g * diff / (delta * delta);
+                    }
                 }
-                deps += -g / (delta * delta);
+                if (p->mean_slot) {
+                    const double* kb = Kb + i * dk;
+                    double delta = dist64_mean(q, kb, dk) + eps;
+                    double A = Smu / Zi;
+                    double dot = 0.0;
+                    for (int d = 0; d < dv; ++d) dot += (double)g_o[d] * (Vb[i * dv + d] - o[d]);
+                    double g = dot / Zi;
+                    gs[i * (k + 1) + k] = g;
+                    ds[i * (k + 1) + k] = delta;
+                    for (int d = 0; d < dv; ++d) dVb[i * dv + d] += A * (double)g_o[d];
+                    for (int d = 0; d < dk; ++d) {
+                        double diff = (double)q[d] - kb[d];
+                        dQ[fi * dk + d] += -2.0 * g * diff / (delta * delta);
+                        dKb[i * dk + d] += 2.0 * g * diff / (delta * delta);
+                    }
+                }
+            }
+            free(o);
+        }
+        /* (2) key side: dv_j, dk_j over the selecting queries in ascending i */
+        #pragma omp parallel
+        {
+            int64_t nt = 1, t = 0;
+#ifdef _OPENMP
+            nt = omp_get_num_threads();
+            t = omp_get_thread_num();
+#endif
+            const int64_t j0 = N * t / nt, j1 = N * (t + 1) / nt;
+            for (int64_t i = 0; i < N; ++i) {
+                if (!(Zs[i] > 0.0)) continue;
+                const int64_t fi = bh * N + i;
+                const float* q = Q + fi * dk;
+                const float* g_o = dO + fi * dv;
+                const int32_t* row = idx + fi * k;
+                for (int r = 0; r < k; ++r) {
+                    const int64_t j = row[r];
+                    if (j < j0 || j >= j1) continue;            /* also skips -1 */
+                    const float* kj = K + (bh * N + j) * dk;
+                    const double g = gs[i * (k + 1) + r], delta = ds[i * (k + 1) + r];
+                    const double A = (1.0 / delta) / Zs[i];
+                    for (int d = 0; d < dv; ++d) dV[(bh * N + j) * dv + d] += A * (double)g_o[d];
+                    for (int d = 0; d < dk; ++d) {
+                        double diff = (double)q[d] - (double)kj[d];
+                        dK[(bh * N + j) * dk + d] += 2.0 * g * diff / (delta * delta);
+                    }
+                }
             }
         }
+        /* deps over (i, slot) ascending, mean slot last within a query */
+        for (int64_t i = 0; i < N; ++i) {
+            if (!(Zs[i] > 0.0)) continue;
+            const int32_t* row = idx + (bh * N + i) * k;
+            for (int r = 0; r < k; ++r) {
+                if (row[r] < 0) continue;
+                const double g = gs[i * (k + 1) + r], delta = ds[i * (k + 1) + r];
+                deps_bh += -g / (delta * delta);
+            }
+            if (p->mean_slot) {
+                const double g = gs[i * (k + 1) + k], delta = ds[i * (k + 1) + k];
+                deps_bh += -g / (delta * delta);
+            }
+        }
+        deps += deps_bh;
         if (p->mean_slot) {
             /* chain rule through the prefix means (S:323(a)):
              *   causal:     dK_t += sum_{i>=t} dKbar_i/(i+1)   (suffix sum, i descending)
@@ -566,14 +637,10 @@ int oref_backward(const oref_problem* p, const float* Q, const float* K, const f
             }
             free(acc);
         }
-        eps_part[bh] = deps;
-        free(o); free(Kb); free(Vb); free(dKb); free(dVb);
     }
     /* D20: one scalar eps per call, gradient summed over all (b,h) in order */
-    double s = 0.0;
-    for (int64_t bh = 0; bh < BH; ++bh) s += eps_part[bh];
-    *d_eps = s;
-    free(eps_part);
+    *d_eps = deps;
+    free(gs); free(ds); free(Zs); free(Kb); free(Vb); free(dKb); free(dVb);
     return OREF_OK;
 }
 

@@ -665,3 +665,126 @@ def test_select_code_invariants_and_d1_exactness():
         d = [abs(int(kc[0, 0, j]) - int(qc[0, 0, i])) for j in row]
         assert d == sorted(d)
         assert set(row) == set(j for j in exact[0, 0, i] if j >= 0)
+
+
+# --------------------------------------------------------------------------- tie rules (D19, D25)
+_TIES = _gold("ties.json")
+
+
+@pytest.mark.parametrize("case", _TIES["euclid"], ids=lambda c: c["cite"][:12])
+def test_select_distance_ties_by_position_golden(case):
+    """D19: candidates at equal distance are ordered (and cut at k) by ascending position j.
+    Hand-worked: every key is a candidate (window covers each run), distances are small exact
+    integers / binary fractions, so the expected rows follow from the (D, j) order alone."""
+    N, dk = case["N"], case["d_k"]
+    Q = np.asarray(case["Q"], np.float32).reshape(1, 1, N, dk)
+    K = np.asarray(case["K"], np.float32).reshape(1, 1, N, dk)
+    for k, want in case["idx_by_k"].items():
+        p = Problem(1, 1, N, dk, 4, int(k), window=case["window"], chunk=case["chunk"], causal=case["causal"])
+        qc, kc, _ = oracle.encode(p, Q, K)
+        sc, pm = oracle.sort(p, kc)
+        idx = oracle.select(p, Q, K, qc, sc, pm)
+        assert idx[0, 0, case["query"]].tolist() == want, (k, case["why"])
+
+
+@pytest.mark.parametrize("case", _TIES["code"], ids=lambda c: c["cite"][:12])
+def test_select_code_ties_by_position_golden(case):
+    """SPEC S:227/S:263 (reading D25): equal |code - query code| -> smaller source index first,
+    across the windows of different runs and within one run (not the sorted-run order)."""
+    N = case["N"]
+    sc = np.asarray(case["scode"], np.uint64).reshape(1, 1, N)
+    pm = np.asarray(case["perm"], np.int32).reshape(1, 1, N)
+    qc = np.asarray(case["qcode"], np.uint64).reshape(1, 1, N)
+    for k, want in case["idx_by_k"].items():
+        p = Problem(1, 1, N, 1, 4, int(k), window=case["window"], chunk=case["chunk"], causal=case["causal"],
+                    mean_slot=0, select=1)
+        idx = oracle.select(p, None, None, qc, sc, pm)
+        assert idx[0, 0, case["query"]].tolist() == want, (k, case["why"])
+
+
+def test_bruteforce_knn_ties_by_position():
+    """The independent brute-force kNN (no Morton) keeps the same (D, j) tie rule (D19)."""
+    case = _TIES["euclid"][0]
+    N, dk = case["N"], case["d_k"]
+    Q = np.asarray(case["Q"], np.float32).reshape(1, 1, N, dk)
+    K = np.asarray(case["K"], np.float32).reshape(1, 1, N, dk)
+    p = Problem(1, 1, N, dk, 4, 4, window=8, causal=0)
+    assert oracle.bruteforce_knn(p, Q, K)[0, 0, 0].tolist() == [0, 2, 3, 5]
+
+
+# --------------------------------------------------------------------------- reading D23 vs the f64 contract
+def _f64_topk_sets(p, Q, K, qc, sc, pm):
+    """Independent f64 selection (numpy): the same candidate windows (insertion point by
+    bisect on the sorted run, D1-D3), ranked by the f64 squared distance, ties by j."""
+    N, M, W, k = p.N, (p.chunk if p.causal else p.N), p.W, p.k
+    q64 = Q[0, 0].astype(np.float64)
+    k64 = K[0, 0].astype(np.float64)
+    sets, kth = [], []
+    for i in range(N):
+        nruns = i // M if p.causal else 1
+        cand = []
+        for c in range(nruns):
+            s0, ln = c * M, min(M, N - c * M)
+            run = [int(x) for x in sc[0, 0, s0:s0 + ln]]
+            ins = bisect.bisect_left(run, int(qc[0, 0, i]))
+            w = min(W, ln)
+            s = min(max(ins - W // 2, 0), ln - w)
+            cand += [int(x) for x in pm[0, 0, s0 + s:s0 + s + w]]
+        cand = np.array(cand, np.int64)
+        if cand.size == 0:
+            sets.append(set()); kth.append(None)
+            continue
+        D = ((k64[cand] - q64[i]) ** 2).sum(axis=1)
+        order = np.lexsort((cand, D))
+        sets.append(set(cand[order[:k]].tolist()))
+        kth.append((D[order[k - 1]], D[order[k]]) if cand.size > k else None)
+    return sets, kth
+
+
+@pytest.mark.parametrize("kind", ["iid", "tokens"])
+def test_f32_ranking_equals_f64_ranking_except_near_ties(kind):
+    """Reading D23 against the north_star contract: the selected SET taken with the pinned f32
+    ranking distance equals the set an f64 ranking gives, except for queries whose f64 k-th and
+    (k+1)-th distances agree within 1e-6 relative (north_star's near-tie clause)."""
+    rng = np.random.default_rng(77 if kind == "iid" else 78)
+    N, dk, k, M, W = 1024, 3, 16, 128, 32
+    p = Problem(1, 1, N, dk, 4, k, window=W, chunk=M, causal=1)
+    if kind == "iid":
+        Q = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+        K = rng.normal(size=(1, 1, N, dk)).astype(np.float32)
+    else:   # repeated tokens: exact duplicate keys (distance ties) and near-duplicate queries
+        E = rng.normal(size=(64, dk)).astype(np.float32)
+        t = rng.integers(0, 64, size=N)
+        K = E[t][None, None]
+        Q = (E[t] + 0.05 * rng.normal(size=(N, dk))).astype(np.float32)[None, None]
+    qc, kc, _ = oracle.encode(p, Q, K)
+    sc, pm = oracle.sort(p, kc)
+    idx = oracle.select(p, Q, K, qc, sc, pm)[0, 0]
+    sets, kth = _f64_topk_sets(p, Q, K, qc, sc, pm)
+    differ = 0
+    for i in range(N):
+        got = set(int(j) for j in idx[i] if j >= 0)
+        if got == sets[i]:
+            continue
+        differ += 1
+        a, b = kth[i]
+        assert abs(b - a) <= 1e-6 * max(abs(a), abs(b)), (i, a, b)
+    assert differ <= N // 50
+
+
+def test_near_tie_clause_is_where_f32_and_f64_differ():
+    """A constructed near-tie: key 0 = (1, 2^-16, 0) is at f64 distance 1 + 2^-32 from q = 0 but at
+    f32 distance exactly 1.0 (the 2^-32 is below half an ulp of 1), key 1 = (1, 0, 0) at exactly 1.
+    f32 ranking ties them and takes j = 0; f64 ranking takes j = 1.  The north_star clause covers
+    exactly this: the f64 k-th and (k+1)-th distances agree within 1e-6 relative."""
+    N = 4
+    K = np.array([[1, 2.0 ** -16, 0], [1, 0, 0], [5, 0, 0], [0, 6, 0]], np.float32).reshape(1, 1, N, 3)
+    Q = np.zeros((1, 1, N, 3), np.float32)
+    p = Problem(1, 1, N, 3, 4, 1, window=8, causal=0)
+    qc, kc, _ = oracle.encode(p, Q, K)
+    sc, pm = oracle.sort(p, kc)
+    assert oracle.select(p, Q, K, qc, sc, pm)[0, 0, 0].tolist() == [0]
+    sets, kth = _f64_topk_sets(p, Q, K, qc, sc, pm)
+    assert sets[0] == {1}
+    a, b = kth[0]
+    assert a == 1.0 and b == 1.0 + 2.0 ** -32 and abs(b - a) <= 1e-6 * b
