@@ -3,11 +3,16 @@
 python bench.py [--gpus N] [--steps K] [--warmup W] [--config long64k] [--impl reference]
 
 A step = one pass of the whole hot path (A1-A12: encode + sort + fwd + bwd)
-over one batch of synthetic input already resident in HBM.  Under torchrun
-every rank runs its OWN batch (weak scaling, one process per GPU, (b,h)
-slices independent -> no data-path collective); the only exchange is the
-shared Cauchy scale's gradient d_eps (one f64 per rank, all-gathered and
-summed in rank order, reading D20).  Rank 0 prints one JSON line.
+over one batch of synthetic input already resident in HBM.  One process per
+GPU: `--gpus N` (N > 1) re-launches this script under torch.distributed.run
+on 127.0.0.1 unless it is already running under it.  (b,h) slices are
+independent problems, so the data path has no collective:
+  --scaling strong (default): the config's B x H slices are split
+      into contiguous per-rank ranges (dist.partition); t_P = max over ranks;
+  --scaling weak: every rank runs the config's whole batch of its own slices.
+The only exchange is the shared Cauchy scale's gradient d_eps (one f64 per
+rank, all-gathered and summed in rank order, reading D20).  Rank 0 prints one
+JSON line.
 
 --impl reference times the CPU oracle (oracle/, the method's plain f64
 reference -- this tier has no installable reference implementation) on the
@@ -165,29 +170,88 @@ def _dist_env():
     return world, rank, local
 
 
-def _make_rank_inputs(cfg, rank):
-    """Each rank's own batch (weak scaling): the config's B x H slices, seeded by global slice id."""
+def rank_slices(cfg, world: int, rank: int, scaling: str):
+    """Global (b,h) slice ids this rank runs and the per-rank problem shape (B', H').
+    strong: contiguous split of the config's B*H slices (SURVEY 8(d) "each rank takes B.H/P
+    contiguous slices"); weak: every rank runs a whole batch of its own slices."""
+    from paper_2501_14577_b200.dist import partition, weak_slices
+    if scaling == "strong":
+        bhs = partition(cfg.BH, world, rank)
+        return bhs, (1, len(bhs))
+    return weak_slices(cfg.BH, rank), (cfg.B, cfg.H)
+
+
+def units_per_step(cfg, world: int, scaling: str) -> int:
+    """Queries every rank together processes in one step."""
+    return cfg.BH * cfg.N * (1 if scaling == "strong" else world)
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    """t_P = max over ranks; identity without a process group."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _make_rank_inputs(cfg, bhs, shape):
+    """This rank's slices (seeded by global slice id, so the ranks' union is the 1-GPU batch)."""
     import numpy as np
 
     import synth
-    from paper_2501_14577_b200.dist import weak_slices
-    bhs = weak_slices(cfg.BH, rank)
     x = synth.make_inputs(cfg, bh_range=bhs)
-    return {n: np.ascontiguousarray(v.reshape(cfg.B, cfg.H, *v.shape[2:])) for n, v in x.items()}
+    return {n: np.ascontiguousarray(v.reshape(*shape, *v.shape[2:])) for n, v in x.items()}
+
+
+def host_info() -> dict:
+    """nproc and the CPU model of this box (every CPU row states them)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.lower().startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 # ----------------------------------------------------------------------------- reference arm (CPU oracle)
+def _oracle_sample(cfg, budget_s: float, max_slices: int):
+    """Run the oracle (as it stands, all host cores) on whole (b,h) slices of the workload, one at
+    a time, until `budget_s` seconds have passed (at least one slice).  -> (seconds, slices)."""
+    import oracle
+    import synth
+    oracle.build()
+    one = cfg.with_(B=1, H=1)
+    p = oracle.Problem(**one.problem_kwargs())
+    sec, n = 0.0, 0
+    while n < max_slices and (n == 0 or sec < budget_s):
+        x = synth.make_inputs(cfg, bh_range=[n])
+        t0 = time.perf_counter()
+        oracle.pipeline(p, x["Q"], x["K"], x["V"], synth.EPS, x["dO"])
+        sec += time.perf_counter() - t0
+        n += 1
+    return sec, n
+
+
 def run_reference(args, cfg, world, rank):
+    """--impl reference: the CPU oracle (this tier's reference arm) on rank 0 only; each step is a
+    bounded sample (one (b,h) slice) of the workload."""
     if rank != 0:
         return
     import oracle
     import synth
     oracle.build()
     one = cfg.with_(B=1, H=1)
-    x = synth.make_inputs(cfg, bh_range=[0])
     p = oracle.Problem(**one.problem_kwargs())
     times = []
     for s in range(args.warmup + args.steps):
+        x = synth.make_inputs(cfg, bh_range=[s % cfg.BH])
         t0 = time.perf_counter()
         oracle.pipeline(p, x["Q"], x["K"], x["V"], synth.EPS, x["dO"])
         dt = time.perf_counter() - t0
@@ -198,76 +262,79 @@ def run_reference(args, cfg, world, rank):
     cores = oracle.num_threads()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_json(cfg, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"one (b,h) slice of {cfg.name} (N={cfg.N} queries) per step, full "
-                                       f"encode+sort+select+fwd+bwd"},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_json(cfg, world, args.scaling),
+            "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                  "sample": f"one (b,h) slice of {cfg.name} (N={cfg.N} queries) per step, full "
+                                            f"encode+sort+select+fwd+bwd"}, **host_info()),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg):
-    """The oracle as it stands on this box's host cores, on a bounded sample: one (b,h) slice."""
+def cpu_baseline(cfg, budget_s: float = 10.0):
+    """The oracle as it stands on this box's host cores, on a bounded sample: whole (b,h) slices of
+    the workload until ~budget_s seconds of oracle time."""
     import oracle
-    import synth
-    oracle.build()
-    one = cfg.with_(B=1, H=1)
-    x = synth.make_inputs(cfg, bh_range=[0])
-    p = oracle.Problem(**one.problem_kwargs())
-    t0 = time.perf_counter()
-    oracle.pipeline(p, x["Q"], x["K"], x["V"], synth.EPS, x["dO"])
-    sec = time.perf_counter() - t0
-    return {"value": cfg.N / sec, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"one (b,h) slice of {cfg.name}: {cfg.N} queries, full encode+sort+select+fwd+bwd, "
-                      f"{sec:.1f} s"}
+    sec, n = _oracle_sample(cfg, budget_s, cfg.BH)
+    return dict({"value": n * cfg.N / sec, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                 "sample": f"{n} of the {cfg.BH} (b,h) slices of {cfg.name} ({n * cfg.N} queries), full "
+                           f"encode+sort+select+fwd+bwd, {sec:.1f} s"}, **host_info())
 
 
-def _config_json(cfg, world):
+def _config_json(cfg, world, scaling):
+    if scaling == "strong":
+        par = f"dp{world}: one process per GPU; the {cfg.BH} (b,h) slices split contiguously over the ranks"
+        gb = cfg.B
+    else:
+        par = f"dp{world}: one process per GPU, each its own batch of {cfg.BH} (b,h) slices"
+        gb = cfg.B * world
     return {"workload": cfg.name, "model": "ZETA top-k attention op (no weights)", "B": cfg.B, "H": cfg.H,
-            "global_batch": cfg.B * world, "seq_len": cfg.N, "d_k": cfg.d_k, "d_v": cfg.d_v, "k": cfg.k,
+            "global_batch": gb, "seq_len": cfg.N, "d_k": cfg.d_k, "d_v": cfg.d_v, "k": cfg.k,
             "window": cfg.window, "chunk": cfg.chunk, "chunks": -(-cfg.N // cfg.chunk) if cfg.causal else 1,
             "causal": cfg.causal, "mean_slot": cfg.mean_slot, "pass": "encode+sort+fwd+bwd",
-            "l2": "inputs larger than L2 (V and dO are 1.6 GB each per GPU at long64k); no flush",
-            "parallelism": f"dp{world}: one process per GPU, each its own batch of (b,h) slices"}
+            "l2": "inputs larger than L2 (V and dO are 1.6 GB each at long64k); no flush",
+            "parallelism": par}
 
 
 # ----------------------------------------------------------------------------- GPU arm
 def run_gpu(args, cfg, world, rank, local):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import __graft_entry__
-    if rank == 0 or world == 1:
+    # bind the device first, then the process group (device_id: NCCL need not guess the rank's GPU)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
         __graft_entry__.build()
     if world > 1:
-        dist.init_process_group("nccl")
-        dist.barrier()
+        dist.barrier(device_ids=[local])
     import paper_2501_14577_b200 as onedf
     from paper_2501_14577_b200 import abi
     from paper_2501_14577_b200 import dist as odist
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    x = _make_rank_inputs(cfg, rank)
+    bhs, (Bp, Hp) = rank_slices(cfg, world, rank, args.scaling)
+    x = _make_rank_inputs(cfg, bhs, (Bp, Hp))
     t = {n: torch.from_numpy(v).to(dev) for n, v in x.items()}
-    p = onedf.make_problem(**cfg.problem_kwargs())
+    p = onedf.make_problem(**dict(cfg.problem_kwargs(), B=Bp, H=Hp))
     import synth
     eps = torch.tensor(synth.EPS, dtype=torch.float32, device=dev)
-    BH, N = cfg.BH, cfg.N
-    qcode = torch.empty((cfg.B, cfg.H, N), dtype=torch.int64, device=dev)
+    N = cfg.N
+    qcode = torch.empty((Bp, Hp, N), dtype=torch.int64, device=dev)
     kcode = torch.empty_like(qcode)
     scode = torch.empty_like(qcode)
-    perm = torch.empty((cfg.B, cfg.H, N), dtype=torch.int32, device=dev)
+    perm = torch.empty((Bp, Hp, N), dtype=torch.int32, device=dev)
     O = torch.empty_like(t["V"])
-    idx = torch.empty((cfg.B, cfg.H, N, cfg.k), dtype=torch.int32, device=dev)
-    Z = torch.empty((cfg.B, cfg.H, N), dtype=torch.float32, device=dev)
+    idx = torch.empty((Bp, Hp, N, cfg.k), dtype=torch.int32, device=dev)
+    Z = torch.empty((Bp, Hp, N), dtype=torch.float32, device=dev)
     dQ, dK, dV = torch.empty_like(t["Q"]), torch.empty_like(t["K"]), torch.empty_like(t["V"])
     d_eps = torch.empty((), dtype=torch.float64, device=dev)
     need = max(onedf.onedf_workspace_size(p, op) for op in (abi.OP_ENCODE, abi.OP_SORT, abi.OP_FWD, abi.OP_BWD))
     wsbuf = torch.empty(need + 256, dtype=torch.uint8, device=dev)
     ws = wsbuf.data_ptr() + ((-wsbuf.data_ptr()) % 256)
+    wsbuf[(-wsbuf.data_ptr()) % 256:][:16].zero_()      # flag words (onedf.h "Errors")
     stream = torch.cuda.current_stream(dev)
 
     # stage events: 0 start | 1 encode | 2 sort | fwd: 3 means 4 records 5 topk | bwd: 6 means 7 CSR
@@ -297,6 +364,10 @@ def run_gpu(args, cfg, world, rank, local):
     stage_names = ["encode", "sort", "fwd_means", "fwd_records", "fwd_topk", "bwd_means", "bwd_transpose",
                    "bwd_query", "bwd_key", "bwd_scans", "bwd_eps", "deps_exchange"]
 
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
     # warm-up
     for _ in range(args.warmup):
         step(new_events())
@@ -312,8 +383,7 @@ def run_gpu(args, cfg, world, rank, local):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         clocks = ClockSampler(gpu_id)
-        if world > 1:
-            dist.barrier()
+        barrier()
         torch.cuda.synchronize(dev)
         clocks.start()
         time.sleep(0.3)
@@ -322,8 +392,7 @@ def run_gpu(args, cfg, world, rank, local):
             step(evs[s])
         t1.record(stream)
         torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
+        barrier()
         clk = clocks.stop()
         total_ms = t0.elapsed_time(t1)
         stages = {n: [] for n in stage_names}
@@ -336,13 +405,11 @@ def run_gpu(args, cfg, world, rank, local):
     if _bad_clocks(clk):
         total_ms, stages, clk = timed()
         clk["remeasured"] = True
-    ms = total_ms / args.steps
-    if world > 1:
-        mt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
-        ms = float(mt.item())
+    ms_rank = total_ms / args.steps
+    ms = max_over_ranks(ms_rank, dev)
 
     launches_per_step = count_launches(p)
+    units = units_per_step(cfg, world, args.scaling)
 
     # ------------------------------------------------------------ e2e through the host-buffer entry point
     e2e = None
@@ -364,8 +431,7 @@ def run_gpu(args, cfg, world, rank, local):
         for _ in range(max(1, min(args.warmup, 2))):
             host_step()
         torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
+        barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         ksteps = max(1, min(args.steps, 5))
@@ -374,30 +440,29 @@ def run_gpu(args, cfg, world, rank, local):
             host_step()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        ems = e0.elapsed_time(e1) / ksteps
-        if world > 1:
-            mt = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(mt, op=dist.ReduceOp.MAX)
-            ems = float(mt.item())
-        e2e = {"value": world * BH * N / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1) / ksteps, dev)
+        e2e = {"value": units / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": onedf.HostStep.h2d_bytes(p), "d2h_bytes_per_step": onedf.HostStep.d2h_bytes(p),
                "api": "onedf_topk_attn_step_host (pinned host buffers, copies inside the timed region)",
                "steps": ksteps}
 
     if rank != 0:
         if world > 1:
-            dist.barrier()
+            barrier()
             dist.destroy_process_group()
         return
 
     # ------------------------------------------------------------ roofline of the dominant kernel
-    ab = alg_bytes(cfg)
+    rcfg = cfg.with_(B=Bp, H=Hp)                      # rank 0's own work (what its events timed)
+    ab = alg_bytes(rcfg)
     peak, peak_src = _peaks()
     kern_map = {"fwd_topk": "fwd_topk", "bwd_query": "bwd_query", "bwd_key": "bwd_key"}
     avg = {n: sum(v) / len(v) for n, v in stages.items()}
     dom = max(kern_map, key=lambda n: avg[n])
     achieved = ab[kern_map[dom]] / (avg[dom] / 1e3) / 1e9
-    traffic = _ncu_traffic(dom)
+    traffic = _ncu_traffic(dom, cfg.name) if (Bp, Hp) == (cfg.B, cfg.H) else None
+    step_dram = _ncu_step_dram(cfg.name) if (Bp, Hp) == (cfg.B, cfg.H) else None
     roof = {"bound": "hbm", "kernel": {"fwd_topk": "topk_attn_fwd_kernel", "bwd_query": "bwd_query_kernel",
                                        "bwd_key": "bwd_key_kernel"}[dom],
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -405,23 +470,28 @@ def run_gpu(args, cfg, world, rank, local):
             "alg_bytes_per_launch": ab[kern_map[dom]], "avg_launch_ms": avg[dom],
             "note": "achieved = SURVEY 8(d) algorithmic bytes (candidate records and gathered rows counted per "
                     "use) / CUDA-event time of the kernel inside the timed region; can exceed 1 only through "
-                    "on-chip (L1/L2) reuse",
-            "step": {"B_alg": ab["B_alg"], "R_alg": ab["B_alg"] / (ms / 1e3) / 1e9 / peak,
-                     "B_comp": ab["B_comp"], "R_comp": ab["B_comp"] / (ms / 1e3) / 1e9 / peak}}
+                    "on-chip (L1/L2) reuse; R_dram = ncu DRAM bytes of every launch of one step (profiles/, "
+                    "measured separately) / this step time",
+            "step": {"B_alg": ab["B_alg"], "R_alg": ab["B_alg"] / (ms_rank / 1e3) / 1e9 / peak,
+                     "B_comp": ab["B_comp"], "R_comp": ab["B_comp"] / (ms_rank / 1e3) / 1e9 / peak,
+                     "B_dram": step_dram,
+                     "R_dram": None if step_dram is None else step_dram / (ms_rank / 1e3) / 1e9 / peak}}
     cpu = None
     if world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg)
-    value = world * BH * N / (ms / 1e3)
+    value = units / (ms / 1e3)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic: seeded iid N(0,1) Q,K,V,dO (synth/, SURVEY 8(d))",
-            "config": _config_json(cfg, world), "tokens_per_s": world * cfg.B * N / (ms / 1e3),
+            "config": _config_json(cfg, world, args.scaling),
+            "tokens_per_s": units / cfg.H / (ms / 1e3),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "gpu_launches_per_step": launches_per_step, "clocks": clk,
+            "rank0_slices": [bhs[0], bhs[-1] + 1] if len(bhs) else [], "rank0_ms_per_step": ms_rank,
             "phases_ms": {n: round(v, 4) for n, v in avg.items()}}
     print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()
+        barrier()
         dist.destroy_process_group()
 
 
@@ -436,15 +506,38 @@ def count_launches(p) -> int:
     return 2 + 1 + fwd + bwd
 
 
-def _ncu_traffic(kernel_key):
-    """dram bytes per launch from the committed ncu --set full summary, if present."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def _ncu_json(name):
     try:
-        with open(path) as f:
-            d = json.load(f)
-        return d.get(kernel_key)
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
     except (OSError, ValueError):
+        return {}
+
+
+def _ncu_traffic(kernel_key, workload):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    d = _ncu_json("ncu_traffic.json")
+    if d.get("workload", "long64k") != workload:
         return None
+    return d.get(kernel_key)
+
+
+def _ncu_step_dram(workload):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum summed over every launch of one step."""
+    d = _ncu_json("ncu_step_dram.json")
+    return d.get("bytes_per_step") if d.get("workload") == workload else None
+
+
+def _self_launch(n: int) -> int:
+    """--gpus N outside torchrun: run N ranks of this script under torch.distributed.run."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -454,13 +547,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="long64k")
     ap.add_argument("--impl", default="onedf", choices=["onedf", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--bh", type=int, default=0, help="override B x H with 1 x BH slices (config sweeps of long N)")
     args = ap.parse_args()
     world, rank, local = _dist_env()
-    if args.gpus is not None and args.gpus != world and world == 1 and args.gpus > 1:
-        print(json.dumps({"error": "run N>1 under torchrun (python -m torch.distributed.run ...)"}))
+    if args.gpus is not None and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _self_launch(args.gpus)
+    if args.gpus is not None and "WORLD_SIZE" in os.environ and args.gpus != world:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}))
         return 1
     import synth
     cfg = synth.CONFIGS[args.config]

@@ -35,9 +35,14 @@
  *                           beyond what this build implements (see validate);
  *   ONEDF_ERR_CUDA          a launch failed (cudaGetLastError).
  *   Data errors detected on the device (non-finite Q/K in encode; eps <= 0 or
- *   non-finite in fwd/bwd) set flag bits in the first 4 bytes of that call's
- *   workspace; onedf_check_device_status(ws) synchronises the stream and
- *   reports them as ONEDF_ERR_NONFINITE.  No exceptions cross the ABI.
+ *   non-finite in fwd/bwd) set flag bits in the workspace header: one 32-bit
+ *   word per op (bytes [4*op, 4*op+4), op = ONEDF_OP_ENCODE .. ONEDF_OP_BWD),
+ *   each zeroed only when that op starts, so one workspace shared by the whole
+ *   pipeline keeps every op's flags until that op runs again.  Zero these 16
+ *   bytes once when a workspace is allocated (the rest of a workspace needs
+ *   no initialisation); onedf_topk_attn_step_host zeroes them itself.
+ *   onedf_check_device_status(ws) synchronises the stream and reports any set
+ *   flag as ONEDF_ERR_NONFINITE.  No exceptions cross the ABI.
  * Determinism.  Every output is bitwise reproducible run to run: no float
  *   atomics anywhere; every reduction has a fixed order.
  */
@@ -119,7 +124,8 @@ onedf_status onedf_validate(const onedf_problem* p);
 int64_t onedf_max_run_length(void);
 
 /* Bytes of device workspace `op` needs (0 if the problem is invalid).  The
- * workspace must be 256-byte aligned; its contents need not be initialised. */
+ * workspace must be 256-byte aligned; apart from the 16-byte flag header (see
+ * "Errors") its contents need not be initialised. */
 size_t onedf_workspace_size(const onedf_problem* p, int op);
 
 /* A1 + A2: bounds and Morton encode (P:952-954 draft C quantiser, Eq. 4
@@ -289,8 +295,9 @@ onedf_status onedf_code_knn(const onedf_problem* p, const uint64_t* qcode, const
 onedf_status onedf_overlap(const int32_t* a, int32_t ka, const int32_t* b, int32_t kb, int64_t rows,
                            int64_t self_period, int32_t* counts, onedf_stream_t stream);
 
-/* Synchronises `stream`, then reads the flag word of `ws` (a workspace
- * previously passed to encode/fwd/bwd): ONEDF_OK or ONEDF_ERR_NONFINITE. */
+/* Synchronises `stream`, then reads the flag words of `ws` (a workspace
+ * previously passed to encode/sort/fwd/bwd; see "Errors"): ONEDF_OK, or
+ * ONEDF_ERR_NONFINITE if any op's flag is set. */
 onedf_status onedf_check_device_status(const void* ws, onedf_stream_t stream);
 
 const char* onedf_status_string(onedf_status s);

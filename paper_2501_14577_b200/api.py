@@ -4,6 +4,8 @@ path runs in libonedf.so's kernels; this file only marshals arguments.
 """
 from __future__ import annotations
 
+import functools
+
 import torch
 
 from . import abi
@@ -24,6 +26,9 @@ def default_chunk(N: int) -> int:
     return 256 if N <= 256 * 32 else -(-N // 32)
 
 
+FLAG_BYTES = 16          # onedf.h "Errors": one 32-bit flag word per op at the start of a workspace
+
+
 class Workspace:
     """A reusable 256-B aligned device byte buffer (grown on demand)."""
 
@@ -36,6 +41,8 @@ class Workspace:
         if self._buf is None or self.nbytes < nbytes:
             self._buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
             self.nbytes = nbytes
+            off = (-self._buf.data_ptr()) % 256
+            self._buf[off:off + FLAG_BYTES].zero_()      # the per-op flag words start cleared (onedf.h "Errors")
         off = (-self._buf.data_ptr()) % 256
         return self._buf.data_ptr() + off, self.nbytes
 
@@ -44,44 +51,77 @@ def _ws(p, op, ws):
     need = abi.onedf_workspace_size(p, op)
     if need == 0:
         raise abi.OnedfError(abi.ERR_INVALID_ARG, "onedf_workspace_size")
-    ws = ws or Workspace()
+    ws = ws or Workspace(torch.device("cuda", torch.cuda.current_device()))
+    if ws.device.index is not None and ws.device.index != torch.cuda.current_device():
+        raise ValueError(f"workspace on {ws.device}, tensors on cuda:{torch.cuda.current_device()}")
     return ws.get(need)
 
 
-def _dev(t: torch.Tensor, dtype=torch.float32):
-    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
-        raise ValueError(f"expected a contiguous CUDA {dtype} tensor, got {t.dtype} on {t.device}")
+def _dev(t: torch.Tensor, dtype=torch.float32, rows: int | None = None, width: int = 1):
+    """A contiguous CUDA tensor of `dtype` holding exactly rows x width elements (rows of `width`
+    in the last dimension): the kernels index it as [rows, width], so a smaller tensor would be
+    read (or written) out of bounds."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise ValueError(f"expected a contiguous CUDA {dtype} tensor, got "
+                         f"{getattr(t, 'dtype', type(t))} on {getattr(t, 'device', '?')}")
+    if rows is not None and (t.numel() != rows * width or (width > 1 and t.shape[-1] != width)):
+        raise ValueError(f"expected {rows} rows of {width} elements, got shape {tuple(t.shape)}")
     return t
 
 
+def _rows(p: Problem) -> int:
+    return p.B * p.H * p.N
+
+
+def _on_one_device(fn):
+    """Run an entry point with the tensors' device current (torch's current stream of that device,
+    and the device the library launches on); all tensor arguments must share one device."""
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        devs = {a.device for a in list(args) + list(kw.values()) if isinstance(a, torch.Tensor)}
+        if len(devs) != 1:
+            raise ValueError(f"all tensor arguments must be on one CUDA device, got {sorted(map(str, devs))}")
+        dev = devs.pop()
+        if dev.type != "cuda":
+            raise ValueError(f"expected CUDA tensors, got {dev}")
+        with torch.cuda.device(dev):
+            return fn(*args, **kw)
+    return wrapper
+
+
+@_on_one_device
 def encode(p: Problem, Q, K, lohi=None, ws: Workspace | None = None):
     """A1+A2 -> (qcode, kcode, lohi); codes are int64 tensors holding the u64 bit patterns."""
-    Q, K = _dev(Q), _dev(K)
+    Q, K = _dev(Q, rows=_rows(p), width=p.d_k), _dev(K, rows=_rows(p), width=p.d_k)
     qcode = torch.empty((p.B, p.H, p.N), dtype=torch.int64, device=Q.device)
     kcode = torch.empty_like(qcode)
     lohi_out = torch.empty((p.B, p.H, 2, p.d_k), dtype=torch.float64, device=Q.device)
     ptr, n = _ws(p, abi.OP_ENCODE, ws)
-    abi.onedf_encode(p, Q, K, None if lohi is None else _dev(lohi, torch.float64), qcode, kcode, lohi_out, ptr, n)
+    lohi = None if lohi is None else _dev(lohi, torch.float64, rows=p.B * p.H * 2, width=p.d_k)
+    abi.onedf_encode(p, Q, K, lohi, qcode, kcode, lohi_out, ptr, n)
     return qcode, kcode, lohi_out
 
 
+@_on_one_device
 def bounds_partial(p: Problem, Q, K, ws: Workspace | None = None):
     """Raw per-(b,h) per-dim min/max over the rows this rank owns -> lohi [B,H,2,d_k] f64 (no widening)."""
-    Q, K = _dev(Q), _dev(K)
+    Q, K = _dev(Q, rows=_rows(p), width=p.d_k), _dev(K, rows=_rows(p), width=p.d_k)
     lohi = torch.empty((p.B, p.H, 2, p.d_k), dtype=torch.float64, device=Q.device)
     ptr, n = _ws(p, abi.OP_ENCODE, ws)
     abi.onedf_bounds_partial(p, Q, K, lohi, ptr, n)
     return lohi
 
 
+@_on_one_device
 def bounds_finish(p: Problem, lohi, ws: Workspace | None = None):
     """Reading D10 in place (hi == lo -> +-0.5); returns lohi."""
-    lohi = _dev(lohi, torch.float64)
+    lohi = _dev(lohi, torch.float64, rows=p.B * p.H * 2, width=p.d_k)
     ptr, n = _ws(p, abi.OP_ENCODE, ws)
     abi.onedf_bounds_finish(p, lohi, ptr, n)
     return lohi
 
 
+@_on_one_device
 def rank_sum(parts):
     """parts [world, ...] f32 -> [...] f32, summed in rank order in f64 (onedf_rank_sum)."""
     parts = _dev(parts)
@@ -90,14 +130,17 @@ def rank_sum(parts):
     return out
 
 
+@_on_one_device
 def code_knn(p: Problem, qcode, scode, perm, exclude_self: bool = False):
     """NEXT-3: k nearest keys by Morton-code distance (ties by position) -> idx [B,H,N,k] int32."""
     idx = torch.empty((p.B, p.H, p.N, p.k), dtype=torch.int32, device=qcode.device)
-    abi.onedf_code_knn(p, _dev(qcode, torch.int64), _dev(scode, torch.int64), _dev(perm, torch.int32), exclude_self,
-                       idx)
+    n = _rows(p)
+    abi.onedf_code_knn(p, _dev(qcode, torch.int64, rows=n), _dev(scode, torch.int64, rows=n),
+                       _dev(perm, torch.int32, rows=n), exclude_self, idx)
     return idx
 
 
+@_on_one_device
 def overlap(a, b, self_period: int = 0):
     """Per row |a ∩ b| (int32 [rows]) of index lists a [..., ka], b [..., kb]; -1 and the row's own
     position (row mod self_period, if > 0) ignored."""
@@ -108,9 +151,10 @@ def overlap(a, b, self_period: int = 0):
     return counts
 
 
+@_on_one_device
 def sort(p: Problem, kcode, ws: Workspace | None = None):
     """A3 -> (scode, perm)."""
-    kcode = _dev(kcode, torch.int64)
+    kcode = _dev(kcode, torch.int64, rows=_rows(p))
     scode = torch.empty_like(kcode)
     perm = torch.empty(kcode.shape, dtype=torch.int32, device=kcode.device)
     ptr, n = _ws(p, abi.OP_SORT, ws)
@@ -118,64 +162,91 @@ def sort(p: Problem, kcode, ws: Workspace | None = None):
     return scode, perm
 
 
+@_on_one_device
 def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | None = None):
     """A4-A7 -> (O, idx, Z)."""
-    Q, K, V, eps = _dev(Q), _dev(K), _dev(V), _dev(eps)
+    n = _rows(p)
+    Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
+    V, eps = _dev(V, rows=n, width=p.d_v), _dev(eps, rows=1)
     O = torch.empty((p.B, p.H, p.N, p.d_v), dtype=torch.float32, device=Q.device)
     idx = torch.empty((p.B, p.H, p.N, p.k), dtype=torch.int32, device=Q.device)
     Z = torch.empty((p.B, p.H, p.N), dtype=torch.float32, device=Q.device)
-    ptr, n = _ws(p, abi.OP_FWD, ws)
-    abi.onedf_topk_attn_fwd(p, Q, K, V, eps, _dev(qcode, torch.int64), _dev(scode, torch.int64),
-                            _dev(perm, torch.int32), O, idx, Z, ptr, n)
+    ptr, nb = _ws(p, abi.OP_FWD, ws)
+    abi.onedf_topk_attn_fwd(p, Q, K, V, eps, _dev(qcode, torch.int64, rows=n), _dev(scode, torch.int64, rows=n),
+                            _dev(perm, torch.int32, rows=n), O, idx, Z, ptr, nb)
     return O, idx, Z
 
 
+@_on_one_device
 def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None, qcode=None, perm=None):
     """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor]).
 
     qcode/perm (optional) only choose the visiting order (Morton schedule); the
     outputs are bitwise identical with or without them."""
-    Q, K, V, eps, O, dO = _dev(Q), _dev(K), _dev(V), _dev(eps), _dev(O), _dev(dO)
+    n = _rows(p)
+    Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
+    V, O, dO = _dev(V, rows=n, width=p.d_v), _dev(O, rows=n, width=p.d_v), _dev(dO, rows=n, width=p.d_v)
+    eps = _dev(eps, rows=1)
     dQ = torch.empty_like(Q)
     dK = torch.empty_like(K)
     dV = torch.empty_like(V)
     d_eps = torch.empty((), dtype=torch.float64, device=Q.device)
-    ptr, n = _ws(p, abi.OP_BWD, ws)
-    qcode = None if qcode is None else _dev(qcode, torch.int64)
-    perm = None if perm is None else _dev(perm, torch.int32)
-    abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32), _dev(Z), qcode, perm, dQ, dK, dV, d_eps,
-                            ptr, n)
+    ptr, nb = _ws(p, abi.OP_BWD, ws)
+    qcode = None if qcode is None else _dev(qcode, torch.int64, rows=n)
+    perm = None if perm is None else _dev(perm, torch.int32, rows=n)
+    abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32, rows=n, width=p.k), _dev(Z, rows=n), qcode,
+                            perm, dQ, dK, dV, d_eps, ptr, nb)
     return dQ, dK, dV, d_eps
 
 
-def check_device_status(ws_ptr: int) -> int:
-    return abi.onedf_check_device_status(ws_ptr)
+def check_device_status(ws) -> int:
+    """Synchronise and read the workspace's device flags (a Workspace or a raw device pointer)."""
+    if isinstance(ws, Workspace):
+        if ws._buf is None:
+            return abi.OK
+        with torch.cuda.device(ws.device):
+            return abi.onedf_check_device_status(ws.get(ws.nbytes)[0])
+    return abi.onedf_check_device_status(ws)
 
 
 class ZetaTopkAttention(torch.autograd.Function):
     """o = ZETA(Q, K, V; eps) with gradients to Q, K, V and eps (indices held fixed, D16)."""
 
     @staticmethod
-    def forward(ctx, Q, K, V, eps, p: Problem):
+    def forward(ctx, Q, K, V, eps, p: Problem, check: bool = False):
         ws = Workspace(Q.device)
         qcode, kcode, _ = encode(p, Q, K, ws=ws)
         scode, perm = sort(p, kcode, ws=ws)
         O, idx, Z = topk_attn_fwd(p, Q, K, V, eps.reshape(()), qcode, scode, perm, ws=ws)
+        if check:
+            _raise_on_flags(ws, "ZetaTopkAttention.forward")
         ctx.save_for_backward(Q, K, V, eps, O, idx, Z, qcode, perm)
         ctx.p = p
+        ctx.check = check
         ctx.mark_non_differentiable(idx)
         return O, idx
 
     @staticmethod
     def backward(ctx, dO, _didx):
         Q, K, V, eps, O, idx, Z, qcode, perm = ctx.saved_tensors
-        dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps.reshape(()), O, dO.contiguous(), idx, Z,
+        ws = Workspace(Q.device)
+        dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps.reshape(()), O, dO.contiguous(), idx, Z, ws=ws,
                                           qcode=qcode, perm=perm)
-        return dQ, dK, dV, d_eps.to(eps.dtype).reshape(eps.shape), None
+        if ctx.check:
+            _raise_on_flags(ws, "ZetaTopkAttention.backward")
+        return dQ, dK, dV, d_eps.to(eps.dtype).reshape(eps.shape), None, None
 
 
-def zeta_attention(Q, K, V, eps, p: Problem):
-    return ZetaTopkAttention.apply(Q, K, V, eps, p)
+def _raise_on_flags(ws: Workspace, where: str):
+    st = check_device_status(ws)           # synchronises the stream
+    if st != abi.OK:
+        raise abi.OnedfError(st, where)
+
+
+def zeta_attention(Q, K, V, eps, p: Problem, check: bool = False):
+    """check=True synchronises after the forward and the backward and raises OnedfError if the
+    device flagged non-finite Q/K or eps <= 0 (opt-in: it costs a stream synchronisation)."""
+    return ZetaTopkAttention.apply(Q, K, V, eps, p, check)
 
 
 class HostStep:

@@ -22,19 +22,12 @@ SOURCES = ["encode.cu", "sort.cu", "mean.cu", "fwd.cu", "bwd.cu", "bwd_dk12.cu",
            "bwd_dk78.cu", "csr.cu", "workload.cu", "abi.cu"]
 
 
-def _stale(out: str, deps) -> bool:
-    if not os.path.exists(out):
-        return True
-    t = os.path.getmtime(out)
-    return any(os.path.getmtime(d) > t for d in deps)
-
-
 def _stamp(files, defines) -> str:
     """Content hash of the sources, headers and flags a library is built from."""
     h = hashlib.sha256()
-    for f in sorted(files):
-        with open(f, "rb") as fh:
-            h.update(f.encode() + b"\0" + fh.read())
+    for f in sorted(files, key=lambda x: os.path.relpath(x, ROOT)):
+        with open(f, "rb") as fh:      # repo-relative names: the same stamp wherever the checkout lives
+            h.update(os.path.relpath(f, ROOT).encode() + b"\0" + fh.read())
     h.update(" ".join(ARCH + FLAGS + list(defines)).encode())
     return h.hexdigest()
 
@@ -65,17 +58,24 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     for src in SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(objdir, src.replace(".cu", ".o"))
-        if force or _stale(o, [s] + hdrs):
+        # per-object content stamp (source + every header + flags + defines): an object is reused
+        # only if it was built from exactly these inputs, whatever the files' mtimes say
+        ostamp = _stamp([s] + hdrs, defines)
+        if force or not os.path.exists(o) or _read(o + ".stamp") != ostamp:
             cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", o]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
-            jobs.append((cmd, o))
+            jobs.append((cmd, o, ostamp))
 
     def run(job):
-        cmd, o = job
+        cmd, o, ostamp = job
+        if os.path.exists(o + ".stamp"):
+            os.remove(o + ".stamp")
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {o}:\n{r.stderr}")
+        with open(o + ".stamp", "w") as f:
+            f.write(ostamp)
         return r.stderr
 
     with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
@@ -83,7 +83,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
             if verbose and log:
                 sys.stderr.write(log)
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _stale(lib, objs) or _read(lib + ".stamp") != stamp:
+    if force or jobs or not os.path.exists(lib) or _read(lib + ".stamp") != stamp:
         cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"]
         subprocess.run(cmd, check=True)
         os.replace(lib + ".tmp", lib)

@@ -154,11 +154,16 @@ static onedf_status pre(const onedf_problem* p, void* ws, size_t ws_bytes, int o
     return check_device();
 }
 
+// Zero the flag word of `op` in the workspace header (common.cuh FLAG_WORDS).
+static cudaError_t zero_flags(void* ws, int op, cudaStream_t st) {
+    return cudaMemsetAsync((char*)ws + 4 * op, 0, 4, st);
+}
+
 // Internal entry points (flag zeroing optional so the host step can chain them).
 static onedf_status do_encode(const onedf_problem* p, const float* Q, const float* K, const double* lohi_in,
                               uint64_t* qcode, uint64_t* kcode, double* lohi_out, void* ws, cudaStream_t st,
                               bool zero) {
-    if (zero && cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+    if (zero && zero_flags(ws, ONEDF_OP_ENCODE, st) != cudaSuccess) return finish(cudaGetLastError());
     Carver c(ws);
     return finish(launch_encode(p, effective_bits(p), Q, K, lohi_in, qcode, kcode, lohi_out, ws, &c, st));
 }
@@ -172,7 +177,7 @@ static onedf_status do_sort(const onedf_problem* p, const uint64_t* kcode, uint6
 static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
                            const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
                            float* Z, void* ws, cudaStream_t st, bool zero, const Trace& tr = Trace()) {
-    if (zero && cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+    if (zero && zero_flags(ws, ONEDF_OP_FWD, st) != cudaSuccess) return finish(cudaGetLastError());
     FwdLayout L = fwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
@@ -184,7 +189,7 @@ static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* 
                            const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
                            const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, void* ws,
                            cudaStream_t st, bool zero, const Trace& tr = Trace()) {
-    if (zero && cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+    if (zero && zero_flags(ws, ONEDF_OP_BWD, st) != cudaSuccess) return finish(cudaGetLastError());
     BwdLayout L = bwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
@@ -232,7 +237,7 @@ onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t*
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_SORT);
     if (s != ONEDF_OK) return s;
     if (!kcode || !scode || !perm) return ONEDF_ERR_INVALID_ARG;
-    if (cudaMemsetAsync(ws, 0, 4, (cudaStream_t)stream) != cudaSuccess) return finish(cudaGetLastError());
+    if (zero_flags(ws, ONEDF_OP_SORT, (cudaStream_t)stream) != cudaSuccess) return finish(cudaGetLastError());
     return do_sort(p, kcode, scode, perm, ws, (cudaStream_t)stream);
 }
 
@@ -313,8 +318,8 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
         e = cudaEventCreateWithFlags(&ev_in[g], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_c[g], cudaEventDisableTiming);
     }
-    if (e == cudaSuccess) e = cudaMemsetAsync(ws, 0, 4, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(sub, 0, 4, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ws, 0, 4 * FLAG_WORDS, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(sub, 0, 4 * FLAG_WORDS, st);
     // eps by value: written by a one-thread kernel so the call needs no host staging buffer
     if (e == cudaSuccess) {
         set_scalar_kernel<<<1, 1, 0, st>>>(L.eps, eps);
@@ -360,7 +365,7 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
     if (s == ONEDF_OK && e == cudaSuccess) {
         sum_groups_kernel<<<1, 1, 0, st>>>(L.d_eps, G);
         e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaMemcpyAsync(ws, sub, 4, cudaMemcpyDeviceToDevice, st);   // surface device flags
+        if (e == cudaSuccess) e = cudaMemcpyAsync(ws, sub, 4 * FLAG_WORDS, cudaMemcpyDeviceToDevice, st);   // surface device flags
         if (e == cudaSuccess) e = cudaMemcpyAsync(d_eps_h, L.d_eps, 8, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaEventRecord(ev_end, sout);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_end, 0);      // the caller's stream covers all copies
@@ -389,7 +394,7 @@ onedf_status onedf_bounds_partial(const onedf_problem* p, const float* Q, const 
     if (s != ONEDF_OK) return s;
     if (!Q || !K || !lohi) return ONEDF_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+    if (zero_flags(ws, ONEDF_OP_ENCODE, st) != cudaSuccess) return finish(cudaGetLastError());
     Carver c(ws);
     return finish(launch_bounds_partial(p, Q, K, lohi, ws, &c, st));
 }
@@ -400,7 +405,7 @@ onedf_status onedf_bounds_finish(const onedf_problem* p, double* lohi, void* ws,
     if (s != ONEDF_OK) return s;
     if (!lohi) return ONEDF_ERR_INVALID_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (cudaMemsetAsync(ws, 0, 4, st) != cudaSuccess) return finish(cudaGetLastError());
+    if (zero_flags(ws, ONEDF_OP_ENCODE, st) != cudaSuccess) return finish(cudaGetLastError());
     return finish(launch_bounds_finish(p, lohi, ws, st));
 }
 
@@ -431,13 +436,15 @@ onedf_status onedf_overlap(const int32_t* a, int32_t ka, const int32_t* b, int32
 
 onedf_status onedf_check_device_status(const void* ws, onedf_stream_t stream) {
     if (!ws) return ONEDF_ERR_INVALID_ARG;
-    unsigned flags = 0;
-    if (cudaMemcpyAsync(&flags, ws, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
+    unsigned flags[FLAG_WORDS] = {0, 0, 0, 0};
+    if (cudaMemcpyAsync(flags, ws, sizeof(flags), cudaMemcpyDeviceToHost, (cudaStream_t)stream) != cudaSuccess ||
         cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) {
         cudaGetLastError();
         return ONEDF_ERR_CUDA;
     }
-    return flags ? ONEDF_ERR_NONFINITE : ONEDF_OK;
+    unsigned any = 0;
+    for (int w = 0; w < FLAG_WORDS; ++w) any |= flags[w];
+    return any ? ONEDF_ERR_NONFINITE : ONEDF_OK;
 }
 
 const char* onedf_status_string(onedf_status s) {

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
     const int64_t gq = bh * N + i;
     const int sc = a.score;
     const float e = __ldg(a.eps);
-    if (sc == SC_CAUCHY && slot == 0 && lane == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, FLAG_BAD_EPS);
+    if (sc == SC_CAUCHY && slot == 0 && lane == 0 && !(e > 0.f && isfinite(e))) set_flag(a.ws, ONEDF_OP_BWD, FLAG_BAD_EPS);
     const double ed = (double)e;
     const int dv = a.dv, k = a.k, nch = dv / 4;
     const int grp = lane / P, l = lane % P;

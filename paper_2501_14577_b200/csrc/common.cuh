@@ -11,8 +11,12 @@ namespace onedf {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int WARP = 32;
 
-// Flag bits written into the first word of a workspace (see onedf.h "Errors").
+// Flag bits written into the header of a workspace (see onedf.h "Errors"):
+// one 32-bit word per op (ONEDF_OP_ENCODE .. ONEDF_OP_BWD), each zeroed only
+// by its own op, so a workspace shared by the whole pipeline keeps every op's
+// flags until that op runs again.
 enum : unsigned { FLAG_NONFINITE_INPUT = 1u, FLAG_BAD_EPS = 2u };
+constexpr int FLAG_WORDS = 4;
 
 // Every workspace starts with this many bytes of header (flag word + pad).
 constexpr size_t WS_HEADER = 256;
@@ -228,8 +232,8 @@ __device__ __forceinline__ double score_raw(int sc, const float* q, const float*
     return -D;
 }
 
-__device__ __forceinline__ void set_flag(void* ws, unsigned bit) {
-    atomicOr((unsigned*)ws, bit);
+__device__ __forceinline__ void set_flag(void* ws, int op, unsigned bit) {
+    atomicOr((unsigned*)ws + op, bit);
 }
 
 }  // namespace onedf

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(ENC_THREADS) bounds_partial_kernel(
             }
         }
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) set_flag(ws, FLAG_NONFINITE_INPUT);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) set_flag(ws, ONEDF_OP_ENCODE, FLAG_NONFINITE_INPUT);
     __shared__ float red[2][DK][ENC_THREADS / 32];
 #pragma unroll
     for (int d = 0; d < DK; ++d) {
@@ -139,7 +139,7 @@ __device__ __forceinline__ uint64_t morton(const float* x, const double* lo, con
     for (int d = 0; d < DK; ++d) {
         double t = __ddiv_rn((double)x[d] - lo[d], hi[d] - lo[d]);
         double g = floor(__dmul_rn(t, top));
-        g = g < 0.0 ? 0.0 : g;            // (NaN falls through; flagged by K1)
+        g = g >= 0.0 ? g : 0.0;           // NaN -> 0 (no undefined cast; the input is flagged by K1)
         g = g > top ? top : g;
         code |= spread<DK>((uint64_t)g, b) << (DK - 1 - d);
     }
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_kernel(
             lo = a; hi = c;
             if (hi == lo) { lo -= 0.5; hi += 0.5; }
         }
-        if (!isfinite(lo) || !isfinite(hi) || !(hi > lo)) set_flag(ws, FLAG_NONFINITE_INPUT);
+        if (!isfinite(lo) || !isfinite(hi) || !(hi > lo)) set_flag(ws, ONEDF_OP_ENCODE, FLAG_NONFINITE_INPUT);
         s_lo[d] = lo; s_hi[d] = hi;
         if (lohi_out && blockIdx.x == 0) {
             lohi_out[bh * 2 * DK + d] = lo;
@@ -268,7 +268,7 @@ __global__ void bounds_finish_kernel(double* __restrict__ lohi, int64_t BH, int 
     const int d = (int)(t % dk);
     double lo = lohi[bh * 2 * dk + d], hi = lohi[bh * 2 * dk + dk + d];
     if (hi == lo) { lo -= 0.5; hi += 0.5; }
-    if (!isfinite(lo) || !isfinite(hi) || !(hi > lo)) set_flag(ws, FLAG_NONFINITE_INPUT);
+    if (!isfinite(lo) || !isfinite(hi) || !(hi > lo)) set_flag(ws, ONEDF_OP_ENCODE, FLAG_NONFINITE_INPUT);
     lohi[bh * 2 * dk + d] = lo;
     lohi[bh * 2 * dk + dk + d] = hi;
 }

@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
     unsigned long long* buf = s_buf[warp];
     const float e = __ldg(a.eps);
     if (a.score == SC_CAUCHY && blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e)))
-        set_flag(a.ws, FLAG_BAD_EPS);
+        set_flag(a.ws, ONEDF_OP_FWD, FLAG_BAD_EPS);
     const double ed = (double)e;
     const int64_t N = a.N;
     const int k = a.k;
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(FWD_THREADS) code_select_attn_kernel(const Fwd
     const int warp = threadIdx.x / 32, lane = lane_id();
     const float e = __ldg(a.eps);
     if (a.score == SC_CAUCHY && blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e)))
-        set_flag(a.ws, FLAG_BAD_EPS);
+        set_flag(a.ws, ONEDF_OP_FWD, FLAG_BAD_EPS);
     const double ed = (double)e;
     const int64_t N = a.N;
     const int k = a.k;

@@ -139,3 +139,57 @@ def test_seqshard_collectives(world):
         torch.testing.assert_close(xg, full, rtol=0, atol=0)                     # every row complete
         torch.testing.assert_close(y, want_sum.float()[:, :, mine], rtol=0, atol=0)  # owner rows summed
         assert s == sum(range(1, world + 1))
+
+
+# ---------------------------------------------------------------- bench harness (strong scaling, max over ranks)
+def _bench_worker(rank, world, port, out):
+    import bench
+    import synth
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.CONFIGS["long64k"]
+    got = {}
+    for scaling in ("strong", "weak"):
+        bhs, shape = bench.rank_slices(cfg, world, rank, scaling)
+        got[scaling] = (list(bhs), shape, bench.units_per_step(cfg, world, scaling))
+    # each rank "times" a different value; every rank must get the max (t_P)
+    got["tmax"] = bench.max_over_ranks(10.0 + 3.0 * rank)
+    out[rank] = got
+    torch.distributed.barrier()
+    torch.distributed.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_rank_partition_and_timing_reduction(world):
+    import synth
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_bench_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    cfg = synth.CONFIGS["long64k"]
+    strong = [out[r]["strong"] for r in range(world)]
+    assert [x for s in strong for x in s[0]] == list(range(cfg.BH))     # contiguous, each slice once
+    assert all(s[1] == (1, len(s[0])) for s in strong)
+    assert all(s[2] == cfg.BH * cfg.N for s in strong)                  # strong: total work fixed
+    weak = [out[r]["weak"] for r in range(world)]
+    assert sorted(x for w in weak for x in w[0]) == list(range(world * cfg.BH))
+    assert all(w[1] == (cfg.B, cfg.H) and w[2] == world * cfg.BH * cfg.N for w in weak)
+    assert all(out[r]["tmax"] == 10.0 + 3.0 * (world - 1) for r in range(world))
+
+
+def test_bench_self_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (torch.distributed.run on
+    127.0.0.1); the reference arm prints one JSON line from rank 0 only."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "tiny", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                       env=env, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["cpu_baseline"]["nproc"] >= 1
