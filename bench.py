@@ -326,6 +326,7 @@ def run_gpu(args, cfg, world, rank, local):
     kcode = torch.empty_like(qcode)
     scode = torch.empty_like(qcode)
     perm = torch.empty((Bp, Hp, N), dtype=torch.int32, device=dev)
+    qorder = torch.empty_like(perm)
     O = torch.empty_like(t["V"])
     idx = torch.empty((Bp, Hp, N, cfg.k), dtype=torch.int32, device=dev)
     Z = torch.empty((Bp, Hp, N), dtype=torch.float32, device=dev)
@@ -352,11 +353,12 @@ def run_gpu(args, cfg, world, rank, local):
         abi.onedf_encode(p, t["Q"], t["K"], None, qcode, kcode, None, ws, need, stream)
         ev[1].record(stream)
         abi.onedf_sort(p, kcode, scode, perm, ws, need, stream)
+        abi.onedf_sort(p, qcode, None, qorder, ws, need, stream)      # Morton query schedule for fwd and bwd
         ev[2].record(stream)
-        abi.onedf_topk_attn_fwd_traced(p, t["Q"], t["K"], t["V"], eps, qcode, scode, perm, O, idx, Z, ws, need,
-                                       ev[3:6], stream)
-        abi.onedf_topk_attn_bwd_traced(p, t["Q"], t["K"], t["V"], eps, O, t["dO"], idx, Z, qcode, perm, dQ, dK, dV,
-                                       d_eps, ws, need, ev[6:12], stream)
+        abi.onedf_topk_attn_fwd_traced(p, t["Q"], t["K"], t["V"], eps, qcode, scode, perm, qorder, O, idx, Z, ws,
+                                       need, ev[3:6], stream)
+        abi.onedf_topk_attn_bwd_traced(p, t["Q"], t["K"], t["V"], eps, O, t["dO"], idx, Z, qcode, qorder, perm, dQ,
+                                       dK, dV, d_eps, ws, need, ev[6:12], stream)
         if world > 1:
             odist.combine_d_eps(d_eps)      # one f64 per rank, rank-ordered sum (D20)
         ev[12].record(stream)
@@ -414,7 +416,7 @@ def run_gpu(args, cfg, world, rank, local):
     # ------------------------------------------------------------ e2e through the host-buffer entry point
     e2e = None
     if not args.no_e2e:
-        del O, idx, Z, dQ, dK, dV, wsbuf, qcode, kcode, scode, perm
+        del O, idx, Z, dQ, dK, dV, wsbuf, qcode, kcode, scode, perm, qorder
         dev_inputs = t
         del dev_inputs, t
         torch.cuda.empty_cache()
@@ -497,13 +499,13 @@ def run_gpu(args, cfg, world, rank, local):
 
 def count_launches(p) -> int:
     """Kernel launches of one step, from the library's launch plan (checked against the ncu launch
-    list in profiles/): encode 2 (bounds partials, encode), sort 1; fwd: prefix means 6 (mean slot),
-    key records 1, Morton query schedule 1, top-k 1; bwd: prefix means 6, CSR count + scan 2, query
-    schedule 1, query side 1, key side 1, mean-slot scans 6, eps 2."""
+    list in profiles/): encode 2 (bounds partials, encode), sort 2 (key runs, Morton query schedule
+    shared by fwd and bwd); fwd: prefix means 6 (mean slot), key records 1, top-k 1; bwd: prefix
+    means 6, CSR count + scan 2, query side 1, key side 1, mean-slot scans 6, eps 2."""
     means = 6 if p.mean_slot else 0
-    fwd = means + 3
-    bwd = means + 2 + 1 + 1 + 1 + means + 2
-    return 2 + 1 + fwd + bwd
+    fwd = means + 2
+    bwd = means + 2 + 1 + 1 + means + 2
+    return 2 + 2 + fwd + bwd
 
 
 def _ncu_json(name):

@@ -15,7 +15,10 @@
  *   The library never allocates, frees or synchronises.
  * Layout.  Contiguous row-major, fastest in the last dimension:
  *   Q, K            float  [B, H, N, d_k]
- *   V, O, dO, dV    float  [B, H, N, d_v]
+ *   V, O, dO, dV    [B, H, N, d_v] of the VALUE STORAGE TYPE p->vdtype:
+ *                   float (ONEDF_DTYPE_F32) or bfloat16 (ONEDF_DTYPE_BF16,
+ *                   SURVEY 8(f) NEXT-4); every sum over them is accumulated in
+ *                   f64 whatever the storage type (reading D26)
  *   qcode, kcode    uint64 [B, H, N]        Morton codes (d_k*b bits used)
  *   scode, perm     uint64 / int32 [B, H, N]  chunk-major sorted runs: run c
  *                   occupies positions [c*M, min((c+1)*M, N)) of each (b,h)
@@ -56,7 +59,7 @@
 extern "C" {
 #endif
 
-#define ONEDF_VERSION 500
+#define ONEDF_VERSION 600
 
 typedef struct CUstream_st* onedf_stream_t;   /* == cudaStream_t */
 
@@ -90,7 +93,17 @@ typedef struct {
     int32_t select;      /* index set of a query (reading D25): ONEDF_SELECT_EUCLID the */
                          /*   exact Euclidean top-k of the candidate windows (D5, the   */
                          /*   method); ONEDF_SELECT_CODE SPEC's code-distance merge      */
+    int32_t vdtype;      /* storage type of V, O, dO, dV (NEXT-4, reading D26):          */
+                         /*   ONEDF_DTYPE_F32 (the method's fp32 contract) or            */
+                         /*   ONEDF_DTYPE_BF16 (halves the gathered row bytes; sums f64) */
 } onedf_problem;
+
+/* Value storage types (onedf_problem.vdtype).  BF16: V and dO are read as
+ * bfloat16 and widened exactly; O and dV are rounded once to bfloat16 (round
+ * to nearest even) from the f64 result.  Q, K, dQ, dK, Z stay float.
+ * Sequence sharding (shard_world > 1) supports F32 only (the partial dV rows
+ * it exchanges would otherwise be rounded per rank). */
+enum { ONEDF_DTYPE_F32 = 0, ONEDF_DTYPE_BF16 = 1 };
 
 /* Score variants: the paper's comparison operators
  * ("Negative Euclidean, Cauchy Softmax ..., and Inverse Euclidean";
@@ -140,9 +153,48 @@ onedf_status onedf_encode(const onedf_problem* p, const float* Q, const float* K
                           const double* lohi_in, uint64_t* qcode, uint64_t* kcode,
                           double* lohi_out, void* ws, size_t ws_bytes, onedf_stream_t stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-4: the upstream projections and the Cauchy scale fused
+ * in front of the encoder.  P:1549 "trainable projection networks f_k and f_q"
+ * map the d_model token features to d_K per head, read as one linear layer
+ * per head (reading D27); "gamma^2 as the output of a sigmoid function
+ * applied to a trainable parameter":
+ *   q_{b,h,n} = Wq[h] x_{b,n} + bq[h],  k_{b,h,n} = Wk[h] x_{b,n} + bk[h],
+ *   eps = sigma(theta) = 1 / (1 + exp(-theta)).
+ * Layouts: X [B, N, d_model] float; Wq, Wk [H, d_k, d_model] float; bq, bk
+ * [H, d_k] float (nullable: no bias); theta device float scalar (nullable: eps
+ * not written); Q, K [B, H, N, d_k] float (outputs, then encoded exactly as by
+ * onedf_encode(Q, K, lohi_in, ...)); eps device float scalar.  Sums are f64
+ * over exact f32 products in a fixed order, one rounding to f32 (bitwise
+ * reproducible).  Non-finite theta sets the ENCODE flag word.
+ * Workspace: onedf_workspace_size(p, ONEDF_OP_ENCODE). */
+onedf_status onedf_project_encode(const onedf_problem* p, int32_t d_model, const float* X,
+                                  const float* Wq, const float* Wk, const float* bq, const float* bk,
+                                  const float* theta, const double* lohi_in, float* Q, float* K,
+                                  float* eps, uint64_t* qcode, uint64_t* kcode, double* lohi_out,
+                                  void* ws, size_t ws_bytes, onedf_stream_t stream);
+
+/* Backward of onedf_project_encode's projections (the codes are constants,
+ * D16): given dQ, dK (onedf_topk_attn_bwd) and d_eps (device double),
+ *   dX = sum_h Wq[h]^T dq + Wk[h]^T dk        [B, N, d_model] (nullable: skipped)
+ *   dWq[h] = sum_{b,n} dq x^T, dWk likewise   [H, d_k, d_model]
+ *   dbq[h] = sum_{b,n} dq, dbk likewise       [H, d_k] (nullable)
+ *   dtheta = d_eps sigma(theta) (1 - sigma(theta))   device float (nullable)
+ * dW/db sum fixed row groups in a fixed order (bitwise reproducible).
+ * Workspace: onedf_project_workspace_size(p, d_model). */
+size_t onedf_project_workspace_size(const onedf_problem* p, int32_t d_model);
+onedf_status onedf_project_bwd(const onedf_problem* p, int32_t d_model, const float* X,
+                               const float* Wq, const float* Wk, const float* theta,
+                               const float* dQ, const float* dK, const double* d_eps, float* dX,
+                               float* dWq, float* dWk, float* dbq, float* dbk, float* dtheta,
+                               void* ws, size_t ws_bytes, onedf_stream_t stream);
+
 /* A3: segmented stable sort of key codes ("torch.sort", "radix
  * sorted", Alg. P:1786-1790 "divide the sorted keys into multiple chunks",
- * S:215-223).  Each run sorted by (code, position); scode/perm chunk-major. */
+ * S:215-223).  Each run sorted by (code, position); scode/perm chunk-major.
+ * scode may be NULL (only the permutation is written).  Applied to the QUERY
+ * codes, perm is the Morton query schedule `qorder` that onedf_topk_attn_fwd
+ * and _bwd accept as a scheduling hint (one sort serves both passes). */
 onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode,
                         int32_t* perm, void* ws, size_t ws_bytes, onedf_stream_t stream);
 
@@ -157,11 +209,16 @@ onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t*
  *   prefix means (D8), Z_i = sum S, o_i = sum (S/Z) v.  Chunk-0 queries with
  *   mean_slot == 0: o = 0, Z = 0, idx = -1 (D7).
  *   eps       device float scalar, eps > 0 and finite (else NONFINITE flag).
+ *   qorder    nullable scheduling hint [B,H,N] int32: onedf_sort's perm of the
+ *             QUERY codes (per chunk, positions by (qcode, i)).  Queries are
+ *             visited in that order (Morton-adjacent queries share candidate
+ *             records and V rows in L1); NULL -> the forward sorts qcode
+ *             itself.  Any per-chunk permutation gives bitwise the same outputs.
  *   O, idx, Z outputs (idx/Z are what onedf_topk_attn_bwd consumes). */
 onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K,
-                                 const float* V, const float* eps, const uint64_t* qcode,
-                                 const uint64_t* scode, const int32_t* perm, float* O,
-                                 int32_t* idx, float* Z, void* ws, size_t ws_bytes,
+                                 const void* V, const float* eps, const uint64_t* qcode,
+                                 const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
+                                 void* O, int32_t* idx, float* Z, void* ws, size_t ws_bytes,
                                  onedf_stream_t stream);
 
 /* A8-A12: backward with I held fixed (D16), appendix P:2006-2045 with the
@@ -177,15 +234,18 @@ onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const f
  *   qcode      nullable scheduling hint: the forward's query codes.  When
  *              given, queries are visited in Morton order per chunk (better
  *              L1 reuse of the gathered V rows); outputs are bitwise the same.
+ *   qorder     nullable scheduling hint: the query schedule itself (onedf_sort
+ *              of qcode, as passed to the forward); wins over qcode and saves
+ *              re-sorting it.  Outputs are bitwise the same.
  *   perm       nullable scheduling hint: onedf_sort's perm.  When given, keys
  *              are visited in sorted-run order; outputs are bitwise the same.
- *   dQ, dK, dV overwritten (f32); d_eps device DOUBLE scalar, overwritten with
+ *   dQ, dK     overwritten (f32); dV overwritten (p->vdtype); d_eps device DOUBLE scalar, overwritten with
  *   the sum over all (b,h,i). */
 onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K,
-                                 const float* V, const float* eps, const float* O,
-                                 const float* dO, const int32_t* idx, const float* Z,
-                                 const uint64_t* qcode, const int32_t* perm,
-                                 float* dQ, float* dK, float* dV, double* d_eps,
+                                 const void* V, const float* eps, const void* O,
+                                 const void* dO, const int32_t* idx, const float* Z,
+                                 const uint64_t* qcode, const int32_t* qorder, const int32_t* perm,
+                                 float* dQ, float* dK, void* dV, double* d_eps,
                                  void* ws, size_t ws_bytes, onedf_stream_t stream);
 
 /* Instrumented twins of the fwd/bwd calls: identical launches and results,
@@ -194,17 +254,20 @@ onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const f
  * caller-created cudaEvent_t handles.  Stages:
  *   fwd: 0 prefix means (A4)  1 sorted key records (K4)  2 top-k attention (A5-A7)
  *   bwd: 0 prefix means (A4)  1 transpose: in-degree CSR (A9)  2 query side (A8)
- *        3 key side (A10)     4 mean-slot scan (A11)      5 eps reduce (A12)    */
+ *        3 key side (A10, incl. the ordering of long CSR segments)  4 mean-slot scan (A11)
+ *        5 eps reduce (A12)    */
 onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K,
-                                        const float* V, const float* eps, const uint64_t* qcode,
-                                        const uint64_t* scode, const int32_t* perm, float* O,
+                                        const void* V, const float* eps, const uint64_t* qcode,
+                                        const uint64_t* scode, const int32_t* perm,
+                                        const int32_t* qorder, void* O,
                                         int32_t* idx, float* Z, void* ws, size_t ws_bytes,
                                         void* const* events, int n_events, onedf_stream_t stream);
 onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K,
-                                        const float* V, const float* eps, const float* O,
-                                        const float* dO, const int32_t* idx, const float* Z,
-                                        const uint64_t* qcode, const int32_t* perm,
-                                        float* dQ, float* dK, float* dV, double* d_eps,
+                                        const void* V, const float* eps, const void* O,
+                                        const void* dO, const int32_t* idx, const float* Z,
+                                        const uint64_t* qcode, const int32_t* qorder,
+                                        const int32_t* perm,
+                                        float* dQ, float* dK, void* dV, double* d_eps,
                                         void* ws, size_t ws_bytes, void* const* events, int n_events,
                                         onedf_stream_t stream);
 
@@ -218,12 +281,15 @@ onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, 
  * computes the current group, so PCIe traffic overlaps the kernels.  Every
  * slice's outputs equal the device path's bit for bit; d_eps is the groups'
  * partial sums added in group order.
+ * V_h, dO_h, O_h, dV_h are of the storage type p->vdtype (bf16 halves their
+ * PCIe bytes).  The query codes are sorted once per group and the schedule
+ * serves both passes.
  * eps is passed by value.  All device buffers live in `ws` (device,
  * onedf_workspace_size(p, ONEDF_OP_STEP_HOST) bytes).  Returns after
  * enqueueing; synchronise `stream` before reading the host outputs. */
 onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h,
-                                       const float* V_h, float eps, const float* dO_h,
-                                       float* O_h, float* dQ_h, float* dK_h, float* dV_h,
+                                       const void* V_h, float eps, const void* dO_h,
+                                       void* O_h, float* dQ_h, float* dK_h, void* dV_h,
                                        double* d_eps_h, void* ws, size_t ws_bytes,
                                        onedf_stream_t stream);
 

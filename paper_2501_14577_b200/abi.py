@@ -20,6 +20,7 @@ OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NONFINITE, ERR_WORKSPACE = r
 OP_ENCODE, OP_SORT, OP_FWD, OP_BWD, OP_STEP_HOST = range(5)
 SCORE_CAUCHY, SCORE_NEG_EUCLID, SCORE_INV_EUCLID, SCORE_DOT = range(4)
 SELECT_EUCLID, SELECT_CODE = range(2)
+DTYPE_F32, DTYPE_BF16 = range(2)
 
 
 class OnedfError(RuntimeError):
@@ -35,7 +36,7 @@ class Problem(ctypes.Structure):
                 ("window", ctypes.c_int32), ("chunk", ctypes.c_int32), ("bits", ctypes.c_int32),
                 ("causal", ctypes.c_int32), ("mean_slot", ctypes.c_int32),
                 ("shard_rank", ctypes.c_int32), ("shard_world", ctypes.c_int32), ("score", ctypes.c_int32),
-                ("select", ctypes.c_int32)]
+                ("select", ctypes.c_int32), ("vdtype", ctypes.c_int32)]
 
     def __repr__(self):
         return "Problem(" + ", ".join(f"{n}={getattr(self, n)}" for n, _ in self._fields_) + ")"
@@ -61,12 +62,16 @@ def _load():
         "onedf_workspace_size": (sz, [P, i32]),
         "onedf_encode": (i32, [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_sort": (i32, [P, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32, vp]),
-        "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp,
-                                             i32, vp]),
+        "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32, vp]),
+        "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz,
+                                             vp, i32, vp]),
         "onedf_topk_attn_step_host": (i32, [P, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_project_encode": (i32, [P, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz,
+                                       vp]),
+        "onedf_project_workspace_size": (sz, [P, ctypes.c_int32]),
+        "onedf_project_bwd": (i32, [P, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_shard_owner": (ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32]),
         "onedf_bounds_partial": (i32, [P, vp, vp, vp, vp, sz, vp]),
         "onedf_bounds_finish": (i32, [P, vp, vp, sz, vp]),
@@ -88,6 +93,7 @@ _lib = _load()
 EXPORTS = ("onedf_validate", "onedf_max_run_length", "onedf_workspace_size", "onedf_encode", "onedf_sort",
            "onedf_topk_attn_fwd", "onedf_topk_attn_bwd", "onedf_topk_attn_fwd_traced",
            "onedf_topk_attn_bwd_traced", "onedf_topk_attn_step_host",
+           "onedf_project_encode", "onedf_project_workspace_size", "onedf_project_bwd",
            "onedf_shard_owner", "onedf_bounds_partial", "onedf_bounds_finish", "onedf_rank_sum",
            "onedf_code_knn", "onedf_overlap",
            "onedf_check_device_status", "onedf_status_string", "onedf_version")
@@ -140,21 +146,24 @@ def onedf_encode(p, Q, K, lohi_in, qcode, kcode, lohi_out, ws, ws_bytes, stream=
 
 
 def onedf_sort(p, kcode, scode, perm, ws, ws_bytes, stream=None):
+    """scode may be None (only perm is written): onedf_sort of the query codes is the query schedule."""
     _check(_lib.onedf_sort(ctypes.byref(p), _p(kcode), _p(scode), _p(perm), _p(ws), ws_bytes, _stream(stream)),
            "onedf_sort")
 
 
-def onedf_topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, ws_bytes, stream=None):
+def onedf_topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, stream=None):
+    """qorder is a nullable scheduling hint (onedf_sort of the query codes); outputs do not depend on it."""
     _check(_lib.onedf_topk_attn_fwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode), _p(perm),
-                                    _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, _stream(stream)),
+                                    _p(qorder), _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, _stream(stream)),
            "onedf_topk_attn_fwd")
 
 
-def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, ws_bytes, stream=None):
-    """qcode/perm are nullable scheduling hints (None -> natural order); outputs do not depend on them."""
+def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws, ws_bytes,
+                        stream=None):
+    """qcode/qorder/perm are nullable scheduling hints (None -> natural order); outputs do not depend on them."""
     _check(_lib.onedf_topk_attn_bwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx), _p(Z),
-                                    _p(qcode), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes,
-                                    _stream(stream)),
+                                    _p(qcode), _p(qorder), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws),
+                                    ws_bytes, _stream(stream)),
            "onedf_topk_attn_bwd")
 
 
@@ -163,19 +172,20 @@ def _events(events):
     return arr, len(events)
 
 
-def onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, ws_bytes, events, stream=None):
+def onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, events,
+                               stream=None):
     arr, n = _events(events)
     _check(_lib.onedf_topk_attn_fwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode),
-                                           _p(perm), _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, arr, n,
+                                           _p(perm), _p(qorder), _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, arr, n,
                                            _stream(stream)), "onedf_topk_attn_fwd_traced")
 
 
-def onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, ws_bytes,
-                               events, stream=None):
+def onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws,
+                               ws_bytes, events, stream=None):
     arr, n = _events(events)
     _check(_lib.onedf_topk_attn_bwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx),
-                                           _p(Z), _p(qcode), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws),
-                                           ws_bytes, arr, n, _stream(stream)), "onedf_topk_attn_bwd_traced")
+                                           _p(Z), _p(qcode), _p(qorder), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps),
+                                           _p(ws), ws_bytes, arr, n, _stream(stream)), "onedf_topk_attn_bwd_traced")
 
 
 def onedf_topk_attn_step_host(p, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_h, dV_h, d_eps_h, ws, ws_bytes,
@@ -184,6 +194,24 @@ def onedf_topk_attn_step_host(p, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_
                                           _p(dQ_h), _p(dK_h), _p(dV_h), _p(d_eps_h), _p(ws), ws_bytes,
                                           _stream(stream)),
            "onedf_topk_attn_step_host")
+
+
+def onedf_project_encode(p, d_model: int, X, Wq, Wk, bq, bk, theta, lohi_in, Q, K, eps, qcode, kcode, lohi_out, ws,
+                         ws_bytes, stream=None):
+    _check(_lib.onedf_project_encode(ctypes.byref(p), d_model, _p(X), _p(Wq), _p(Wk), _p(bq), _p(bk), _p(theta),
+                                     _p(lohi_in), _p(Q), _p(K), _p(eps), _p(qcode), _p(kcode), _p(lohi_out), _p(ws),
+                                     ws_bytes, _stream(stream)), "onedf_project_encode")
+
+
+def onedf_project_workspace_size(p: Problem, d_model: int) -> int:
+    return _lib.onedf_project_workspace_size(ctypes.byref(p), d_model)
+
+
+def onedf_project_bwd(p, d_model: int, X, Wq, Wk, theta, dQ, dK, d_eps, dX, dWq, dWk, dbq, dbk, dtheta, ws, ws_bytes,
+                      stream=None):
+    _check(_lib.onedf_project_bwd(ctypes.byref(p), d_model, _p(X), _p(Wq), _p(Wk), _p(theta), _p(dQ), _p(dK),
+                                  _p(d_eps), _p(dX), _p(dWq), _p(dWk), _p(dbq), _p(dbk), _p(dtheta), _p(ws), ws_bytes,
+                                  _stream(stream)), "onedf_project_bwd")
 
 
 def onedf_shard_owner(chunk: int, world: int) -> int:

@@ -13,8 +13,10 @@ from .abi import Problem
 
 
 def make_problem(B, H, N, d_k, d_v, k, window=0, chunk=1, bits=0, causal=1, mean_slot=1, shard_rank=0,
-                 shard_world=1, score=0, select=0) -> Problem:
-    p = Problem(B, H, N, d_k, d_v, k, window, chunk, bits, causal, mean_slot, shard_rank, shard_world, score, select)
+                 shard_world=1, score=0, select=0, vdtype=0) -> Problem:
+    """vdtype: storage type of V, O, dO, dV -- abi.DTYPE_F32 (0) or abi.DTYPE_BF16 (1) (NEXT-4, reading D26)."""
+    p = Problem(B, H, N, d_k, d_v, k, window, chunk, bits, causal, mean_slot, shard_rank, shard_world, score, select,
+                vdtype)
     st = abi.onedf_validate(p)
     if st != abi.OK:
         raise abi.OnedfError(st, "onedf_validate")
@@ -71,6 +73,11 @@ def _dev(t: torch.Tensor, dtype=torch.float32, rows: int | None = None, width: i
 
 def _rows(p: Problem) -> int:
     return p.B * p.H * p.N
+
+
+def value_dtype(p: Problem) -> torch.dtype:
+    """torch dtype of the value rows V, O, dO, dV of a problem (onedf_problem.vdtype)."""
+    return torch.bfloat16 if p.vdtype == abi.DTYPE_BF16 else torch.float32
 
 
 def _on_one_device(fn):
@@ -163,29 +170,45 @@ def sort(p: Problem, kcode, ws: Workspace | None = None):
 
 
 @_on_one_device
-def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | None = None):
-    """A4-A7 -> (O, idx, Z)."""
+def query_schedule(p: Problem, qcode, ws: Workspace | None = None):
+    """The Morton query schedule: onedf_sort of the query codes (perm only) -> qorder [B,H,N] int32.
+    Passing it to topk_attn_fwd and topk_attn_bwd saves each of them sorting qcode."""
+    qcode = _dev(qcode, torch.int64, rows=_rows(p))
+    qorder = torch.empty(qcode.shape, dtype=torch.int32, device=qcode.device)
+    ptr, n = _ws(p, abi.OP_SORT, ws)
+    abi.onedf_sort(p, qcode, None, qorder, ptr, n)
+    return qorder
+
+
+@_on_one_device
+def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | None = None, qorder=None):
+    """A4-A7 -> (O, idx, Z).  V and O are of value_dtype(p); qorder (optional) is the query schedule
+    (query_schedule), which only chooses the visiting order: outputs are bitwise the same without it."""
     n = _rows(p)
     Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
-    V, eps = _dev(V, rows=n, width=p.d_v), _dev(eps, rows=1)
-    O = torch.empty((p.B, p.H, p.N, p.d_v), dtype=torch.float32, device=Q.device)
+    V, eps = _dev(V, value_dtype(p), rows=n, width=p.d_v), _dev(eps, rows=1)
+    qorder = None if qorder is None else _dev(qorder, torch.int32, rows=n)
+    O = torch.empty((p.B, p.H, p.N, p.d_v), dtype=value_dtype(p), device=Q.device)
     idx = torch.empty((p.B, p.H, p.N, p.k), dtype=torch.int32, device=Q.device)
     Z = torch.empty((p.B, p.H, p.N), dtype=torch.float32, device=Q.device)
     ptr, nb = _ws(p, abi.OP_FWD, ws)
     abi.onedf_topk_attn_fwd(p, Q, K, V, eps, _dev(qcode, torch.int64, rows=n), _dev(scode, torch.int64, rows=n),
-                            _dev(perm, torch.int32, rows=n), O, idx, Z, ptr, nb)
+                            _dev(perm, torch.int32, rows=n), qorder, O, idx, Z, ptr, nb)
     return O, idx, Z
 
 
 @_on_one_device
-def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None, qcode=None, perm=None):
-    """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor]).
+def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None, qcode=None, perm=None,
+                  qorder=None):
+    """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor]); V, O, dO, dV of value_dtype(p).
 
-    qcode/perm (optional) only choose the visiting order (Morton schedule); the
+    qcode/qorder/perm (optional) only choose the visiting order (Morton schedule); the
     outputs are bitwise identical with or without them."""
     n = _rows(p)
+    vt = value_dtype(p)
     Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
-    V, O, dO = _dev(V, rows=n, width=p.d_v), _dev(O, rows=n, width=p.d_v), _dev(dO, rows=n, width=p.d_v)
+    V, O, dO = (_dev(V, vt, rows=n, width=p.d_v), _dev(O, vt, rows=n, width=p.d_v),
+                _dev(dO, vt, rows=n, width=p.d_v))
     eps = _dev(eps, rows=1)
     dQ = torch.empty_like(Q)
     dK = torch.empty_like(K)
@@ -193,10 +216,56 @@ def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None 
     d_eps = torch.empty((), dtype=torch.float64, device=Q.device)
     ptr, nb = _ws(p, abi.OP_BWD, ws)
     qcode = None if qcode is None else _dev(qcode, torch.int64, rows=n)
+    qorder = None if qorder is None else _dev(qorder, torch.int32, rows=n)
     perm = None if perm is None else _dev(perm, torch.int32, rows=n)
     abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32, rows=n, width=p.k), _dev(Z, rows=n), qcode,
-                            perm, dQ, dK, dV, d_eps, ptr, nb)
+                            qorder, perm, dQ, dK, dV, d_eps, ptr, nb)
     return dQ, dK, dV, d_eps
+
+
+@_on_one_device
+def project_encode(p: Problem, X, Wq, Wk, bq=None, bk=None, theta=None, lohi=None, ws: Workspace | None = None):
+    """NEXT-4: q = Wq[h] x + bq[h], k = Wk[h] x + bk[h] (reading D27) and eps = sigma(theta)
+    (P:1361), then the encoder -> (Q, K, eps | None, qcode, kcode, lohi).
+    X [B, N, d_model]; Wq, Wk [H, d_k, d_model]; bq, bk [H, d_k] or None; theta a scalar tensor or None."""
+    dm = X.shape[-1]
+    X = _dev(X, rows=p.B * p.N, width=dm)
+    Wq, Wk = _dev(Wq, rows=p.H * p.d_k, width=dm), _dev(Wk, rows=p.H * p.d_k, width=dm)
+    bq = None if bq is None else _dev(bq, rows=p.H * p.d_k)
+    bk = None if bk is None else _dev(bk, rows=p.H * p.d_k)
+    theta = None if theta is None else _dev(theta, rows=1)
+    lohi = None if lohi is None else _dev(lohi, torch.float64, rows=p.B * p.H * 2, width=p.d_k)
+    Q = torch.empty((p.B, p.H, p.N, p.d_k), dtype=torch.float32, device=X.device)
+    K = torch.empty_like(Q)
+    eps = torch.empty((), dtype=torch.float32, device=X.device) if theta is not None else None
+    qcode = torch.empty((p.B, p.H, p.N), dtype=torch.int64, device=X.device)
+    kcode = torch.empty_like(qcode)
+    lohi_out = torch.empty((p.B, p.H, 2, p.d_k), dtype=torch.float64, device=X.device)
+    ptr, n = _ws(p, abi.OP_ENCODE, ws)
+    abi.onedf_project_encode(p, dm, X, Wq, Wk, bq, bk, theta, lohi, Q, K, eps, qcode, kcode, lohi_out, ptr, n)
+    return Q, K, eps, qcode, kcode, lohi_out
+
+
+@_on_one_device
+def project_bwd(p: Problem, X, Wq, Wk, dQ, dK, theta=None, d_eps=None, need_dX: bool = True, bias: bool = True,
+                ws: Workspace | None = None):
+    """Backward of project_encode -> (dX | None, dWq, dWk, dbq | None, dbk | None, dtheta | None)."""
+    dm = X.shape[-1]
+    X = _dev(X, rows=p.B * p.N, width=dm)
+    Wq, Wk = _dev(Wq, rows=p.H * p.d_k, width=dm), _dev(Wk, rows=p.H * p.d_k, width=dm)
+    dQ, dK = _dev(dQ, rows=_rows(p), width=p.d_k), _dev(dK, rows=_rows(p), width=p.d_k)
+    theta = None if theta is None else _dev(theta, rows=1)
+    d_eps = None if d_eps is None else _dev(d_eps, torch.float64, rows=1)
+    dX = torch.empty_like(X) if need_dX else None
+    dWq, dWk = torch.empty_like(Wq), torch.empty_like(Wk)
+    dbq = torch.empty((p.H, p.d_k), dtype=torch.float32, device=X.device) if bias else None
+    dbk = torch.empty_like(dbq) if bias else None
+    dtheta = torch.empty((), dtype=torch.float32, device=X.device) if theta is not None and d_eps is not None else None
+    need = abi.onedf_project_workspace_size(p, dm)
+    ws = ws or Workspace(X.device)
+    ptr, n = ws.get(need)
+    abi.onedf_project_bwd(p, dm, X, Wq, Wk, theta, dQ, dK, d_eps, dX, dWq, dWk, dbq, dbk, dtheta, ptr, n)
+    return dX, dWq, dWk, dbq, dbk, dtheta
 
 
 def check_device_status(ws) -> int:
@@ -217,10 +286,11 @@ class ZetaTopkAttention(torch.autograd.Function):
         ws = Workspace(Q.device)
         qcode, kcode, _ = encode(p, Q, K, ws=ws)
         scode, perm = sort(p, kcode, ws=ws)
-        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps.reshape(()), qcode, scode, perm, ws=ws)
+        qorder = query_schedule(p, qcode, ws=ws)          # one Morton schedule for both passes
+        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps.reshape(()), qcode, scode, perm, ws=ws, qorder=qorder)
         if check:
             _raise_on_flags(ws, "ZetaTopkAttention.forward")
-        ctx.save_for_backward(Q, K, V, eps, O, idx, Z, qcode, perm)
+        ctx.save_for_backward(Q, K, V, eps, O, idx, Z, qorder, perm)
         ctx.p = p
         ctx.check = check
         ctx.mark_non_differentiable(idx)
@@ -228,10 +298,10 @@ class ZetaTopkAttention(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, dO, _didx):
-        Q, K, V, eps, O, idx, Z, qcode, perm = ctx.saved_tensors
+        Q, K, V, eps, O, idx, Z, qorder, perm = ctx.saved_tensors
         ws = Workspace(Q.device)
         dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps.reshape(()), O, dO.contiguous(), idx, Z, ws=ws,
-                                          qcode=qcode, perm=perm)
+                                          qorder=qorder, perm=perm)
         if ctx.check:
             _raise_on_flags(ws, "ZetaTopkAttention.backward")
         return dQ, dK, dV, d_eps.to(eps.dtype).reshape(eps.shape), None, None
@@ -241,6 +311,40 @@ def _raise_on_flags(ws: Workspace, where: str):
     st = check_device_status(ws)           # synchronises the stream
     if st != abi.OK:
         raise abi.OnedfError(st, where)
+
+
+class ZetaProjectedAttention(torch.autograd.Function):
+    """The attention core of a ZETA layer from token features: x -> (f_q, f_k, sigma) -> top-k
+    Cauchy attention over V (NEXT-4 fused front end + the hot path); gradients to X, Wq, Wk, bq,
+    bk, theta and V (indices and codes held fixed, D16)."""
+
+    @staticmethod
+    def forward(ctx, X, Wq, Wk, bq, bk, theta, V, p: Problem):
+        ws = Workspace(X.device)
+        Q, K, eps, qcode, kcode, _ = project_encode(p, X, Wq, Wk, bq, bk, theta.reshape(()), ws=ws)
+        scode, perm = sort(p, kcode, ws=ws)
+        qorder = query_schedule(p, qcode, ws=ws)
+        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, ws=ws, qorder=qorder)
+        ctx.save_for_backward(X, Wq, Wk, theta, V, Q, K, eps, O, idx, Z, qorder, perm)
+        ctx.p = p
+        ctx.has_bias = (bq is not None, bk is not None)
+        ctx.mark_non_differentiable(idx)
+        return O, idx
+
+    @staticmethod
+    def backward(ctx, dO, _didx):
+        X, Wq, Wk, theta, V, Q, K, eps, O, idx, Z, qorder, perm = ctx.saved_tensors
+        ws = Workspace(X.device)
+        dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps, O, dO.contiguous(), idx, Z, ws=ws, qorder=qorder,
+                                          perm=perm)
+        dX, dWq, dWk, dbq, dbk, dth = project_bwd(ctx.p, X, Wq, Wk, dQ, dK, theta.reshape(()), d_eps, ws=ws)
+        return (dX, dWq, dWk, dbq if ctx.has_bias[0] else None, dbk if ctx.has_bias[1] else None,
+                dth.to(theta.dtype).reshape(theta.shape), dV, None)
+
+
+def zeta_projected_attention(X, Wq, Wk, bq, bk, theta, V, p: Problem):
+    """O, idx = ZETA attention of V with q, k = f_q(X), f_k(X) and eps = sigma(theta) (NEXT-4)."""
+    return ZetaProjectedAttention.apply(X, Wq, Wk, bq, bk, theta, V, p)
 
 
 def zeta_attention(Q, K, V, eps, p: Problem, check: bool = False):
@@ -264,8 +368,10 @@ class HostStep:
 
     @staticmethod
     def h2d_bytes(p: Problem) -> int:
-        return 4 * p.BH * p.N * (2 * p.d_k + 2 * p.d_v)
+        ev = value_dtype(p).itemsize
+        return p.BH * p.N * (4 * 2 * p.d_k + ev * 2 * p.d_v)
 
     @staticmethod
     def d2h_bytes(p: Problem) -> int:
-        return 4 * p.BH * p.N * (2 * p.d_k + 2 * p.d_v) + 8
+        ev = value_dtype(p).itemsize
+        return p.BH * p.N * (4 * 2 * p.d_k + ev * 2 * p.d_v) + 8

@@ -18,8 +18,16 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
          "--fmad=true", "-I", INCLUDE, "-I", CSRC]
-SOURCES = ["encode.cu", "sort.cu", "mean.cu", "fwd.cu", "bwd.cu", "bwd_dk12.cu", "bwd_dk34.cu", "bwd_dk56.cu",
-           "bwd_dk78.cu", "csr.cu", "workload.cu", "abi.cu"]
+SOURCES = ["fwd_inst.cu", "bwd_inst.cu", "encode.cu", "sort.cu", "mean.cu", "fwd.cu", "bwd.cu", "csr.cu",
+           "proj.cu", "workload.cu", "abi.cu"]
+# Compilation units: (object, source, unit defines).  The kernel-template instantiation sources are
+# compiled once per unit (value storage type x register rows / d_k pair) so the instantiations build in parallel;
+# heaviest first.
+UNITS = ([(f"fwd_{n}_r{r}", "fwd_inst.cu", (f"ONEDF_INST_TV={tv}", f"ONEDF_INST_TV_{tv.upper()}", f"ONEDF_INST_R={r}"))
+          for r in (8, 4, 2, 1) for n, tv in (("f32", "float"), ("bf16", "bf16"))]
+         + [(f"bwd_{n}_dk{a}{b}", "bwd_inst.cu", (f"ONEDF_INST_TV={tv}", f"ONEDF_INST_DK_A={a}", f"ONEDF_INST_DK_B={b}"))
+            for n, tv in (("f32", "float"), ("bf16", "bf16")) for a, b in ((1, 2), (3, 4), (5, 6), (7, 8))]
+         + [(src[:-3], src, ()) for src in SOURCES if not src.endswith("_inst.cu")])
 
 
 def _stamp(files, defines) -> str:
@@ -55,14 +63,14 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
     if not force and not defines and _read(lib + ".stamp") == stamp and os.path.exists(lib):
         return lib          # built from exactly these sources and flags (objects need not be present)
     jobs = []
-    for src in SOURCES:
+    for obj, src, udefs in UNITS:
         s = os.path.join(CSRC, src)
-        o = os.path.join(objdir, src.replace(".cu", ".o"))
+        o = os.path.join(objdir, obj + ".o")
         # per-object content stamp (source + every header + flags + defines): an object is reused
         # only if it was built from exactly these inputs, whatever the files' mtimes say
-        ostamp = _stamp([s] + hdrs, defines)
+        ostamp = _stamp([s] + hdrs, tuple(defines) + tuple(udefs))
         if force or not os.path.exists(o) or _read(o + ".stamp") != ostamp:
-            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in tuple(defines) + tuple(udefs)], "-c", s, "-o", o]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((cmd, o, ostamp))
@@ -82,7 +90,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
         for log in ex.map(run, jobs):
             if verbose and log:
                 sys.stderr.write(log)
-    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+    objs = [os.path.join(objdir, obj + ".o") for obj, _, _ in UNITS]
     if force or jobs or not os.path.exists(lib) or _read(lib + ".stamp") != stamp:
         cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"]
         subprocess.run(cmd, check=True)

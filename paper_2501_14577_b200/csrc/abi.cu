@@ -59,9 +59,11 @@ static onedf_status validate(const onedf_problem* p) {
     if (p->shard_world < 0 || p->shard_world > 4096) return ONEDF_ERR_INVALID_ARG;
     if (p->score < ONEDF_SCORE_CAUCHY || p->score > ONEDF_SCORE_DOT) return ONEDF_ERR_INVALID_ARG;
     if (p->select != ONEDF_SELECT_EUCLID && p->select != ONEDF_SELECT_CODE) return ONEDF_ERR_INVALID_ARG;
+    if (p->vdtype != ONEDF_DTYPE_F32 && p->vdtype != ONEDF_DTYPE_BF16) return ONEDF_ERR_INVALID_ARG;
     if (p->shard_world > 1) {
         if (p->shard_rank < 0 || p->shard_rank >= p->shard_world) return ONEDF_ERR_INVALID_ARG;
         if (!p->causal) return ONEDF_ERR_UNSUPPORTED;   // sequence sharding is defined over causal chunks
+        if (p->vdtype != ONEDF_DTYPE_F32) return ONEDF_ERR_UNSUPPORTED;   // partial dV rows are exchanged in f32
     } else if (p->shard_rank != 0) {
         return ONEDF_ERR_INVALID_ARG;
     }
@@ -105,12 +107,14 @@ static size_t sort_bytes(const onedf_problem* p) {
 constexpr int STEP_GROUPS_MAX = 8;
 
 struct StepLayout {
-    float *Q, *K, *V, *dO, *O, *dQ, *dK, *dV, *Z, *eps;
+    float *Q, *K, *dQ, *dK, *Z, *eps;
+    char *V, *dO, *O, *dV;          // value rows of the storage type p->vdtype
     double* d_eps;
     uint64_t *qcode, *kcode, *scode;
-    int32_t *perm, *idx;
+    int32_t *perm, *qorder, *idx;
     size_t sub_off, sub_bytes, bytes;
 };
+static size_t value_bytes(const onedf_problem* p) { return p->vdtype == ONEDF_DTYPE_BF16 ? 2 : 4; }
 static StepLayout step_layout(const onedf_problem* p, void* ws) {
     StepLayout L;
     const size_t e = encode_bytes(p), s = sort_bytes(p);
@@ -119,12 +123,13 @@ static StepLayout step_layout(const onedf_problem* p, void* ws) {
     sub = sub > f ? sub : f;
     sub = sub > b ? sub : b;
     Carver c(ws);
-    const int64_t BH = p->B * p->H, N = p->N, nk = BH * N * p->d_k, nv = BH * N * p->d_v;
-    L.Q = c.take<float>(nk); L.K = c.take<float>(nk); L.V = c.take<float>(nv); L.dO = c.take<float>(nv);
-    L.O = c.take<float>(nv); L.dQ = c.take<float>(nk); L.dK = c.take<float>(nk); L.dV = c.take<float>(nv);
+    const int64_t BH = p->B * p->H, N = p->N, nk = BH * N * p->d_k;
+    const size_t nvb = (size_t)(BH * N * p->d_v) * value_bytes(p);
+    L.Q = c.take<float>(nk); L.K = c.take<float>(nk); L.V = c.take<char>(nvb); L.dO = c.take<char>(nvb);
+    L.O = c.take<char>(nvb); L.dQ = c.take<float>(nk); L.dK = c.take<float>(nk); L.dV = c.take<char>(nvb);
     L.Z = c.take<float>(BH * N); L.eps = c.take<float>(1); L.d_eps = c.take<double>(STEP_GROUPS_MAX + 1);
     L.qcode = c.take<uint64_t>(BH * N); L.kcode = c.take<uint64_t>(BH * N); L.scode = c.take<uint64_t>(BH * N);
-    L.perm = c.take<int32_t>(BH * N); L.idx = c.take<int32_t>(BH * N * p->k);
+    L.perm = c.take<int32_t>(BH * N); L.qorder = c.take<int32_t>(BH * N); L.idx = c.take<int32_t>(BH * N * p->k);
     c.take<char>(0);
     L.sub_off = c.off;
     L.sub_bytes = sub;
@@ -167,27 +172,28 @@ static onedf_status do_encode(const onedf_problem* p, const float* Q, const floa
     Carver c(ws);
     return finish(launch_encode(p, effective_bits(p), Q, K, lohi_in, qcode, kcode, lohi_out, ws, &c, st));
 }
-static onedf_status do_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode, int32_t* perm,
-                            void* ws, cudaStream_t st) {
+static onedf_status do_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode /* nullable */,
+                            int32_t* perm, void* ws, cudaStream_t st) {
     Carver c(ws);
     SortScratch scr;
     sort_carve(p, &c, &scr);
     return finish(launch_seg_sort(p, kcode, scode, perm, scr, st));
 }
-static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                           const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
-                           float* Z, void* ws, cudaStream_t st, bool zero, const Trace& tr = Trace()) {
+static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
+                           const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
+                           void* O, int32_t* idx, float* Z, void* ws, cudaStream_t st, bool zero,
+                           const Trace& tr = Trace()) {
     if (zero && zero_flags(ws, ONEDF_OP_FWD, st) != cudaSuccess) return finish(cudaGetLastError());
     FwdLayout L = fwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
     tr.mark(0, st);
-    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, &L.m, &L.f, ws, st, tr);
+    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, &L.m, &L.f, ws, st, tr);
     return finish(e);
 }
-static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                           const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
-                           const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, void* ws,
+static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
+                           const void* dO, const int32_t* idx, const uint64_t* qcode, const int32_t* qorder,
+                           const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, void* ws,
                            cudaStream_t st, bool zero, const Trace& tr = Trace()) {
     if (zero && zero_flags(ws, ONEDF_OP_BWD, st) != cudaSuccess) return finish(cudaGetLastError());
     BwdLayout L = bwd_layout(p, ws);
@@ -195,7 +201,7 @@ static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* 
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
     tr.mark(0, st);
     if (e == cudaSuccess)
-        e = launch_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st, tr);
+        e = launch_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st, tr);
     return finish(e);
 }
 
@@ -236,67 +242,70 @@ onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t*
                         size_t ws_bytes, onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_SORT);
     if (s != ONEDF_OK) return s;
-    if (!kcode || !scode || !perm) return ONEDF_ERR_INVALID_ARG;
+    if (!kcode || !perm) return ONEDF_ERR_INVALID_ARG;
     if (zero_flags(ws, ONEDF_OP_SORT, (cudaStream_t)stream) != cudaSuccess) return finish(cudaGetLastError());
     return do_sort(p, kcode, scode, perm, ws, (cudaStream_t)stream);
 }
 
-onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V,
+// value-row pointers: 16-B aligned (float4 chunks) for float rows, 8-B (4 x bf16) for bf16 rows
+static bool rows_misaligned(const onedf_problem* p, const void* a, const void* b, const void* c = nullptr) {
+    const uintptr_t m = p->vdtype == ONEDF_DTYPE_BF16 ? 7 : 15;
+    return ((((uintptr_t)a) | ((uintptr_t)b) | ((uintptr_t)c)) & m) != 0;
+}
+
+onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                  const float* eps, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,
-                                 float* O, int32_t* idx, float* Z, void* ws, size_t ws_bytes, onedf_stream_t stream) {
-    onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_FWD);
-    if (s != ONEDF_OK) return s;
-    if (!Q || !K || !V || !eps || !qcode || !scode || !perm || !O || !idx || !Z) return ONEDF_ERR_INVALID_ARG;
-    if ((((uintptr_t)V) | ((uintptr_t)O)) & 15) return ONEDF_ERR_INVALID_ARG;
-    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, (cudaStream_t)stream, true);
+                                 const int32_t* qorder, void* O, int32_t* idx, float* Z, void* ws, size_t ws_bytes,
+                                 onedf_stream_t stream) {
+    return onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, nullptr,
+                                      0, stream);
 }
 
-onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V,
-                                 const float* eps, const float* O, const float* dO, const int32_t* idx,
-                                 const float* Z, const uint64_t* qcode, const int32_t* perm, float* dQ, float* dK,
-                                 float* dV, double* d_eps, void* ws, size_t ws_bytes, onedf_stream_t stream) {
-    onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_BWD);
-    if (s != ONEDF_OK) return s;
-    if (!Q || !K || !V || !eps || !O || !dO || !idx || !Z || !dQ || !dK || !dV || !d_eps)
-        return ONEDF_ERR_INVALID_ARG;
-    if ((((uintptr_t)V) | ((uintptr_t)dO) | ((uintptr_t)dV)) & 15) return ONEDF_ERR_INVALID_ARG;
-    return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true);
+onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V,
+                                 const float* eps, const void* O, const void* dO, const int32_t* idx, const float* Z,
+                                 const uint64_t* qcode, const int32_t* qorder, const int32_t* perm, float* dQ,
+                                 float* dK, void* dV, double* d_eps, void* ws, size_t ws_bytes,
+                                 onedf_stream_t stream) {
+    return onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws,
+                                      ws_bytes, nullptr, 0, stream);
 }
 
-onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K, const float* V,
+onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                         const float* eps, const uint64_t* qcode, const uint64_t* scode,
-                                        const int32_t* perm, float* O, int32_t* idx, float* Z, void* ws,
-                                        size_t ws_bytes, void* const* events, int n_events, onedf_stream_t stream) {
+                                        const int32_t* perm, const int32_t* qorder, void* O, int32_t* idx, float* Z,
+                                        void* ws, size_t ws_bytes, void* const* events, int n_events,
+                                        onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_FWD);
     if (s != ONEDF_OK) return s;
     if (!Q || !K || !V || !eps || !qcode || !scode || !perm || !O || !idx || !Z) return ONEDF_ERR_INVALID_ARG;
-    if ((((uintptr_t)V) | ((uintptr_t)O)) & 15) return ONEDF_ERR_INVALID_ARG;
+    if (rows_misaligned(p, V, O)) return ONEDF_ERR_INVALID_ARG;
     Trace tr;
     tr.ev = events;
     tr.n = n_events;
-    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, O, idx, Z, ws, (cudaStream_t)stream, true, tr);
+    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, (cudaStream_t)stream, true, tr);
 }
 
-onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K, const float* V,
-                                        const float* eps, const float* O, const float* dO, const int32_t* idx,
-                                        const float* Z, const uint64_t* qcode, const int32_t* perm, float* dQ,
-                                        float* dK, float* dV, double* d_eps, void* ws, size_t ws_bytes,
-                                        void* const* events, int n_events, onedf_stream_t stream) {
+onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K, const void* V,
+                                        const float* eps, const void* O, const void* dO, const int32_t* idx,
+                                        const float* Z, const uint64_t* qcode, const int32_t* qorder,
+                                        const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, void* ws,
+                                        size_t ws_bytes, void* const* events, int n_events, onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_BWD);
     if (s != ONEDF_OK) return s;
+    // O and Z are part of the interface but not read (reading R3: recomputed in f64)
     if (!Q || !K || !V || !eps || !O || !dO || !idx || !Z || !dQ || !dK || !dV || !d_eps)
         return ONEDF_ERR_INVALID_ARG;
-    if ((((uintptr_t)V) | ((uintptr_t)dO) | ((uintptr_t)dV)) & 15) return ONEDF_ERR_INVALID_ARG;
+    if (rows_misaligned(p, V, dO, dV)) return ONEDF_ERR_INVALID_ARG;
     Trace tr;
     tr.ev = events;
     tr.n = n_events;
-    return do_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, perm, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true,
+    return do_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true,
                   tr);
 }
 
-onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h, const float* V_h,
-                                       float eps, const float* dO_h, float* O_h, float* dQ_h, float* dK_h,
-                                       float* dV_h, double* d_eps_h, void* ws, size_t ws_bytes,
+onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h, const void* V_h,
+                                       float eps, const void* dO_h, void* O_h, float* dQ_h, float* dK_h,
+                                       void* dV_h, double* d_eps_h, void* ws, size_t ws_bytes,
                                        onedf_stream_t stream) {
     if (validate(p) == ONEDF_OK && p->shard_world > 1) return ONEDF_ERR_UNSUPPORTED;   // needs the caller's collectives
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_STEP_HOST);
@@ -334,12 +343,15 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
         onedf_problem pg = *p;
         pg.B = 1;
         pg.H = nh;
-        const size_t ok = (size_t)(h0 * N * p->d_k), ov = (size_t)(h0 * N * p->d_v), o1 = (size_t)(h0 * N);
-        const size_t bk = (size_t)(nh * N * p->d_k) * 4, bv = (size_t)(nh * N * p->d_v) * 4;
+        const size_t es = value_bytes(p);
+        const size_t ok = (size_t)(h0 * N * p->d_k), ov = (size_t)(h0 * N * p->d_v) * es, o1 = (size_t)(h0 * N);
+        const size_t bk = (size_t)(nh * N * p->d_k) * 4, bv = (size_t)(nh * N * p->d_v) * es;
+        const char* Vh = static_cast<const char*>(V_h);
+        const char* dOh = static_cast<const char*>(dO_h);
         e = cudaMemcpyAsync(L.Q + ok, Q_h + ok, bk, cudaMemcpyHostToDevice, sin);
         if (e == cudaSuccess) e = cudaMemcpyAsync(L.K + ok, K_h + ok, bk, cudaMemcpyHostToDevice, sin);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(L.V + ov, V_h + ov, bv, cudaMemcpyHostToDevice, sin);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(L.dO + ov, dO_h + ov, bv, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(L.V + ov, Vh + ov, bv, cudaMemcpyHostToDevice, sin);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(L.dO + ov, dOh + ov, bv, cudaMemcpyHostToDevice, sin);
         if (e == cudaSuccess) e = cudaEventRecord(ev_in[g], sin);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_in[g], 0);
         if (e != cudaSuccess) break;
@@ -347,19 +359,21 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
             ONEDF_OK)
             break;
         if ((s = do_sort(&pg, L.kcode + o1, L.scode + o1, L.perm + o1, sub, st)) != ONEDF_OK) break;
-        if ((s = do_fwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.qcode + o1, L.scode + o1, L.perm + o1, L.O + ov,
-                        L.idx + o1 * p->k, L.Z + o1, sub, st, false)) != ONEDF_OK)
+        // the Morton query schedule, sorted once for both passes
+        if ((s = do_sort(&pg, L.qcode + o1, nullptr, L.qorder + o1, sub, st)) != ONEDF_OK) break;
+        if ((s = do_fwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.qcode + o1, L.scode + o1, L.perm + o1,
+                        L.qorder + o1, L.O + ov, L.idx + o1 * p->k, L.Z + o1, sub, st, false)) != ONEDF_OK)
             break;
-        if ((s = do_bwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.O + ov, L.dO + ov, L.idx + o1 * p->k, L.Z + o1,
-                        L.qcode + o1, L.perm + o1, L.dQ + ok, L.dK + ok, L.dV + ov, L.d_eps + 1 + g, sub, st,
+        if ((s = do_bwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.dO + ov, L.idx + o1 * p->k, L.qcode + o1,
+                        L.qorder + o1, L.perm + o1, L.dQ + ok, L.dK + ok, L.dV + ov, L.d_eps + 1 + g, sub, st,
                         false)) != ONEDF_OK)
             break;
         e = cudaEventRecord(ev_c[g], st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev_c[g], 0);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(O_h + ov, L.O + ov, bv, cudaMemcpyDeviceToHost, sout);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(static_cast<char*>(O_h) + ov, L.O + ov, bv, cudaMemcpyDeviceToHost, sout);
         if (e == cudaSuccess) e = cudaMemcpyAsync(dQ_h + ok, L.dQ + ok, bk, cudaMemcpyDeviceToHost, sout);
         if (e == cudaSuccess) e = cudaMemcpyAsync(dK_h + ok, L.dK + ok, bk, cudaMemcpyDeviceToHost, sout);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(dV_h + ov, L.dV + ov, bv, cudaMemcpyDeviceToHost, sout);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(static_cast<char*>(dV_h) + ov, L.dV + ov, bv, cudaMemcpyDeviceToHost, sout);
         h0 += nh;
     }
     if (s == ONEDF_OK && e == cudaSuccess) {
@@ -381,6 +395,43 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
     if (sout) cudaStreamDestroy(sout);
     if (s != ONEDF_OK) return s;
     return finish(e);
+}
+
+onedf_status onedf_project_encode(const onedf_problem* p, int32_t d_model, const float* X, const float* Wq,
+                                  const float* Wk, const float* bq, const float* bk, const float* theta,
+                                  const double* lohi_in, float* Q, float* K, float* eps, uint64_t* qcode,
+                                  uint64_t* kcode, double* lohi_out, void* ws, size_t ws_bytes,
+                                  onedf_stream_t stream) {
+    if (validate(p) == ONEDF_OK && p->shard_world > 1 && !lohi_in) return ONEDF_ERR_INVALID_ARG;
+    onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_ENCODE);
+    if (s != ONEDF_OK) return s;
+    if (d_model < 1 || !X || !Wq || !Wk || !Q || !K || !qcode || !kcode || (theta && !eps)) return ONEDF_ERR_INVALID_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (zero_flags(ws, ONEDF_OP_ENCODE, st) != cudaSuccess) return finish(cudaGetLastError());
+    cudaError_t e = launch_project(p, d_model, X, Wq, Wk, bq, bk, theta, Q, K, eps, ws, st);
+    if (e != cudaSuccess) return finish(e);
+    return do_encode(p, Q, K, lohi_in, qcode, kcode, lohi_out, ws, st, false);
+}
+
+size_t onedf_project_workspace_size(const onedf_problem* p, int32_t d_model) {
+    if (validate(p) != ONEDF_OK || d_model < 1) return 0;
+    Carver c(nullptr);
+    return project_ws_bytes(p, d_model, &c);
+}
+
+onedf_status onedf_project_bwd(const onedf_problem* p, int32_t d_model, const float* X, const float* Wq,
+                               const float* Wk, const float* theta, const float* dQ, const float* dK,
+                               const double* d_eps, float* dX, float* dWq, float* dWk, float* dbq, float* dbk,
+                               float* dtheta, void* ws, size_t ws_bytes, onedf_stream_t stream) {
+    onedf_status s = validate(p);
+    if (s != ONEDF_OK) return s;
+    if (d_model < 1) return ONEDF_ERR_INVALID_ARG;
+    if (!ws || (((uintptr_t)ws) & 255) != 0 || ws_bytes < onedf_project_workspace_size(p, d_model))
+        return ONEDF_ERR_WORKSPACE;
+    if ((s = check_device()) != ONEDF_OK) return s;
+    if (!X || !Wq || !Wk || !dQ || !dK || !dWq || !dWk || (dtheta && (!theta || !d_eps))) return ONEDF_ERR_INVALID_ARG;
+    return finish(launch_project_bwd(p, d_model, X, Wq, Wk, theta, dQ, dK, d_eps, dX, dWq, dWk, dbq, dbk, dtheta, ws,
+                                     (cudaStream_t)stream));
 }
 
 int32_t onedf_shard_owner(int64_t chunk, int32_t world) {

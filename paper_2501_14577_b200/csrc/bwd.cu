@@ -26,7 +26,8 @@
 // key's CSR segment (integer cursor, csr.cu).
 // K9: one warp per key j (keys visited in sorted-run order when perm is
 // given) orders its CSR segment by query position (register bitonic sort of
-// (i << 8 | position) keys up to 256 entries, rank counting beyond), then
+// (i << 8 | position) keys up to 256 entries; longer segments were ordered by
+// csr.cu's bitmap counting sort after the query side), then
 // walks it 32 entries at a time: lane groups of P gather the dO_i rows into
 // f64 accumulators, a fixed shuffle tree at the end -- a deterministic
 // segment reduction, no float atomics.  Every per-row result is independent
@@ -41,6 +42,7 @@ void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b) {
     b->eps_q = c->take<double>((size_t)total);
     b->eps_part = c->take<double>((size_t)EPS_PARTS);
     b->qorder = c->take<int32_t>((size_t)total);
+    b->dV32 = p->vdtype == ONEDF_DTYPE_BF16 ? c->take<float>((size_t)(total * p->d_v)) : nullptr;
     sort_carve(p, c, &b->scr);
 }
 
@@ -82,14 +84,14 @@ static int lanes_per_row(int dv) {
     return P;
 }
 
-cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                       const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
-                       const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, const MeanBufs* m,
+cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
+                       const void* dO, const int32_t* idx, const uint64_t* qcode, const int32_t* qorder,
+                       const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, const MeanBufs* m,
                        BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
     cudaError_t e = cudaSuccess;
-    const int32_t* qorder = nullptr;
-    if (qcode) {
+    if (!qorder && qcode) {
+        // schedule hint given as codes only: sort them here (the forward's qorder saves this)
         e = launch_query_order(p, qcode, b->qorder, b->scr, st);
         if (e != cudaSuccess) return e;
         qorder = b->qorder;
@@ -99,10 +101,10 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     if (e != cudaSuccess) return e;
     tr.mark(1, st);
     BwdArgs a;
-    a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.O = O; a.dO = dO; a.idx = idx; a.Z = Z;
+    a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.dO = dO; a.idx = idx;
     a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.qorder = qorder;
     a.dQ = dQ; a.muco = b->muco; a.eps_q = b->eps_q;
-    a.cursor = t->cursor; a.rec = t->rec; a.L = N * (int64_t)p->k;
+    a.cursor = t->cursor; a.rec_i = t->rec_i; a.rec_aw = t->rec_aw; a.L = N * (int64_t)p->k;
     a.sh = make_shard(p);
     a.nq = a.sh.slots(N);
     a.N = N; a.total = BH * a.nq; a.k = p->k; a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
@@ -118,19 +120,31 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
     const int nch = p->d_v / 4;
     const unsigned qgrid = (unsigned)((a.total + BWD_WARPS - 1) / BWD_WARPS);
     const unsigned kgrid = (unsigned)((total + BWD_WARPS - 1) / BWD_WARPS);
-    ONEDF_DISPATCH_DK(p->d_k, { launch_bwd_query_dk<DK>(a, P, nch, p->d_v, p->k, qgrid, st); });
+    ONEDF_DISPATCH_TV(p->vdtype, {
+        ONEDF_DISPATCH_DK(p->d_k, { launch_bwd_query_dk<DK, TV>(a, P, nch, p->d_v, p->k, qgrid, st); });
+    });
     tr.mark(2, st);
+    // the ascending-i order of the long segments (hub keys), now that every record is in place
+    e = launch_csr_long_order(p, t, st);
+    if (e != cudaSuccess) return e;
     KeyArgs ka;
-    ka.Q = Q; ka.K = K; ka.dO = dO; ka.offsets = t->offsets; ka.rec = t->rec;
+    ka.Q = Q; ka.K = K; ka.dO = dO; ka.offsets = t->offsets; ka.rec_i = t->rec_i; ka.rec_aw = t->rec_aw;
     ka.order = t->order;
     ka.korder = perm;
-    ka.dK = dK; ka.dV = dV; ka.N = N; ka.L = N * (int64_t)p->k; ka.total = total; ka.k = p->k; ka.dv = p->d_v;
+    // the key side's dV in f32: the output itself (float rows) or the f32 scratch of a BF16 problem
+    float* dV32 = p->vdtype == ONEDF_DTYPE_BF16 ? b->dV32 : static_cast<float*>(dV);
+    ka.dK = dK; ka.dV = dV32; ka.N = N; ka.L = N * (int64_t)p->k; ka.total = total; ka.k = p->k; ka.dv = p->d_v;
     ka.kt = p->score == SC_DOT ? 0.0 : 1.0;
-    ONEDF_DISPATCH_DK(p->d_k, { launch_bwd_key_dk<DK>(ka, P, p->d_v, kgrid, st); });
+    ONEDF_DISPATCH_TV(p->vdtype, {
+        ONEDF_DISPATCH_DK(p->d_k, { launch_bwd_key_dk<DK, TV>(ka, P, p->d_v, kgrid, st); });
+    });
     tr.mark(3, st);
     if (p->mean_slot) {
         e = launch_mean_grad_scan(p, Q, dO, reinterpret_cast<const float*>(b->muco), const_cast<MeanBufs*>(m), dK,
-                                  dV, st);
+                                  dV32, dV, st);
+        if (e != cudaSuccess) return e;
+    } else if (p->vdtype == ONEDF_DTYPE_BF16) {
+        e = launch_round_rows(dV32, static_cast<bf16*>(dV), total * p->d_v, st);
         if (e != cudaSuccess) return e;
     }
     tr.mark(4, st);

@@ -1,6 +1,6 @@
 // bwd_kernels.cuh -- the A8 query-side (K7) and A10 key-side (K9) kernel
-// templates, shared by the per-d_k instantiation units bwd_dk*.cu (split so
-// the many (d_k, lanes-per-row, registers) instantiations compile in
+// templates, shared by the per-(d_k, storage type) instantiation units of bwd_inst.cu
+// (the many (d_k, lanes-per-row, registers) instantiations compile in
 // parallel) and by bwd.cu, which holds the launch sequence.  See bwd.cu for
 // the method and citations.
 #pragma once
@@ -20,11 +20,11 @@ constexpr int BWD_THREADS = BWD_WARPS * 32;
 #endif
 
 struct BwdArgs {
-    const float* Q; const float* K; const float* V; const float* eps;
-    const float* O; const float* dO; const int32_t* idx; const float* Z;
+    const float* Q; const float* K; const void* V; const float* eps;     // V, dO: storage type TV (vdtype)
+    const void* dO; const int32_t* idx;
     const float* Kbar; const float* Vbar; const int32_t* qorder;
     float* dQ; float2* muco; double* eps_q;
-    int32_t* cursor; int4* rec;                           // key-major CSR records (csr.cu)
+    int32_t* cursor; int32_t* rec_i; float2* rec_aw;      // key-major CSR records (csr.cu, SoA)
     int64_t N, total, nq, L;        // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
     int k, dv, causal, mean_slot, score;
     Shard sh;
@@ -80,7 +80,7 @@ __device__ __forceinline__ void slot_w(int sc, const float* q, const float* kj, 
     }
 }
 
-template <int DK, int P, int CH, int R, bool WHOLE>
+template <int DK, int P, int CH, int R, bool WHOLE, typename TV>
 __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(const BwdArgs a) {
     constexpr int G = 32 / P;                    // rows per step
     constexpr int T = P < 8 ? P : 8;             // steps per block (live partials / loads in flight per lane)
@@ -121,11 +121,10 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
 #pragma unroll
     for (int h = 0; h < CH; ++h) {
         const int ch = l + h * P;
-        g4[h] = ch < nch ? __ldg(reinterpret_cast<const float4*>(a.dO + gq * dv) + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+        g4[h] = ch < nch ? ld4(static_cast<const TV*>(a.dO) + gq * dv, ch) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const int64_t mrow = a.causal ? i : 0;
-    const float* Vb = a.V + bh * N * (int64_t)dv;
-    const float4* V4 = reinterpret_cast<const float4*>(Vb);
+    const TV* Vb = static_cast<const TV*>(a.V) + bh * N * (int64_t)dv;
     const int owner_t = l >> (LOGP - LOGT);
     const bool owner = (l & ((1 << (LOGP - LOGT)) - 1)) == 0;
     double* sp = s_part[warp];
@@ -143,15 +142,17 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
             for (int t = 0; t < T; ++t) {
                 const int j = __shfl_sync(FULL, jr[r], (h0 + t * G + grp) & 31);
                 // an unselected slot (j < 0) reads row 0; its dot is never used (phase 2 skips it)
-                const float4* vr = V4 + (int64_t)(j < 0 ? 0 : j) * nch + l;
+                const TV* vr = Vb + (int64_t)(j < 0 ? 0 : j) * dv;
 #pragma unroll
                 for (int h = 0; h < CH; ++h) {
-                    if (WHOLE) x[t][h] = __ldg(vr + h * P);            // P*CH == d_v/4: every chunk exists
-                    else x[t][h] = l + h * P < nch ? __ldg(vr + h * P) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (WHOLE) x[t][h] = ld4(vr, l + h * P);            // P*CH == d_v/4: every chunk exists
+                    else x[t][h] = l + h * P < nch ? ld4(vr, l + h * P) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
 #pragma unroll
             for (int t = 0; t < T; ++t) {
+                // exact f32 products summed in f64: these dots enter g = (dO.v_j - c)/Z, whose
+                // cancellation when one weight dominates would amplify any rounding here (R3, R5)
                 part[t] = 0.0;
 #pragma unroll
                 for (int h = 0; h < CH; ++h) {
@@ -234,7 +235,8 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
     for (int d = 0; d < DK; ++d) dq[d] = 0.0;
     double deps = 0.0;
     int32_t* cur = a.cursor + bh * N;
-    int4* rec = a.rec + bh * a.L;
+    int32_t* rec_i = a.rec_i + bh * a.L;
+    float2* rec_aw = a.rec_aw + bh * a.L;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int e2 = r * 32 + lane;
@@ -251,7 +253,8 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
             deps += de;
             // append the record to key j's CSR segment (integer slot; the key side orders by i)
             const int32_t pos = atomicAdd(cur + jr[r], 1);
-            rec[pos] = make_int4((int32_t)i, __float_as_int((float)A), __float_as_int((float)w), 0);
+            rec_i[pos] = (int32_t)i;
+            rec_aw[pos] = make_float2((float)A, (float)w);
         }
     }
     if (a.mean_slot) {
@@ -280,8 +283,8 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
 }
 
 struct KeyArgs {
-    const float* Q; const float* K; const float* dO;
-    const int32_t* offsets; const int4* rec; int32_t* order;
+    const float* Q; const float* K; const void* dO;        // dO: storage type TV; dK, dV written as f32
+    const int32_t* offsets; const int32_t* rec_i; const float2* rec_aw; const int32_t* order;
     const int32_t* korder;
     float* dK; float* dV;
     int64_t N, L, total;
@@ -289,8 +292,6 @@ struct KeyArgs {
     double kt;           // dk += w (q - kt k): 1 for the distance scores, 0 for DOT
 };
 
-constexpr int KEY_REG_SEG = 256;      // segments up to this length are ordered in registers
-constexpr int KEY_POS_BITS = 8;       // u32 sort key (i << 8 | position): needs N < 2^24
 
 template <int R>
 __device__ __forceinline__ void sort_prefix(uint32_t (&x)[8]) {
@@ -302,7 +303,7 @@ __device__ __forceinline__ void sort_prefix(uint32_t (&x)[8]) {
     for (int r = 0; r < R; ++r) x[r] = y[r];
 }
 
-template <int DK, int P, int CH>
+template <int DK, int P, int CH, typename TV>
 __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(const KeyArgs a) {
     constexpr int G = 32 / P;
     constexpr int U = ONEDF_KEY_U;                // entries per lane group in flight
@@ -316,7 +317,8 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
     const int32_t* off = a.offsets + bh * (N + 1);
     const int32_t s0 = __ldg(off + j), s1 = __ldg(off + j + 1);
     const int32_t len = s1 - s0;
-    const int4* rec = a.rec + bh * a.L + s0;
+    const int32_t* ri = a.rec_i + bh * a.L + s0;
+    const float2* raw = a.rec_aw + bh * a.L + s0;
     const int dv = a.dv, nch = dv / 4;
     const int grp = lane / P, l = lane % P;
     if (len == 0) {
@@ -329,15 +331,15 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
     }
 
     // ---- fixed visiting order: ascending query position i (distinct within a segment)
-    const bool small = len <= KEY_REG_SEG && N < (1ll << (32 - KEY_POS_BITS));
+    const bool small = !csr_long_segment(len, N);
     uint32_t* sk = s_key[warp];                   // sorted (i << 8 | position) keys
-    int32_t* go = a.order + bh * a.L + s0;
+    const int32_t* go = a.order + bh * a.L + s0;
     if (small) {
         uint32_t xs[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             const int e = r * 32 + lane;
-            xs[r] = e < len ? ((uint32_t)__ldg(&rec[e].x) << KEY_POS_BITS) | (uint32_t)e : ~0u;
+            xs[r] = e < len ? ((uint32_t)__ldg(ri + e) << KEY_POS_BITS) | (uint32_t)e : ~0u;
         }
         if (len <= 32) sort_prefix<1>(xs);
         else if (len <= 64) sort_prefix<2>(xs);
@@ -347,15 +349,8 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
         for (int r = 0; r < 8; ++r)
             if (r * 32 < len) sk[r * 32 + lane] = xs[r];
         __syncwarp();
-    } else {
-        for (int e = lane; e < len; e += 32) {
-            const int32_t mine = __ldg(&rec[e].x);
-            int rank = 0;
-            for (int x = 0; x < len; ++x) rank += __ldg(&rec[x].x) < mine;
-            go[rank] = e;
-        }
-        __syncwarp();
     }
+    // long segments were ordered beforehand by csr_long_order_kernel into `order` (go)
 
     float kj[DK];
 #pragma unroll
@@ -368,7 +363,7 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
     for (int h = 0; h < CH; ++h)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[h][c] = 0.0;
-    const float* dOb = a.dO + bh * N * (int64_t)dv;
+    const TV* dOb = static_cast<const TV*>(a.dO) + bh * N * (int64_t)dv;
     const float* Qb = a.Q + bh * N * DK;
 
     for (int32_t b0 = 0; b0 < len; b0 += 32) {
@@ -384,11 +379,10 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
                 e = (int)(v & ((1u << KEY_POS_BITS) - 1));
                 iq = (int)(v >> KEY_POS_BITS);
             } else {
-                e = go[t];
-                iq = __ldg(&rec[e].x);
+                e = __ldg(go + t);
+                iq = __ldg(ri + e);
             }
-            const int4 rv = __ldg(rec + e);
-            aw = make_float2(__int_as_float(rv.y), __int_as_float(rv.z));
+            aw = __ldg(raw + e);
 #pragma unroll
             for (int d = 0; d < DK; ++d) qi[d] = __ldg(Qb + (int64_t)iq * DK + d);
         }
@@ -407,20 +401,18 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
 #pragma unroll
                 for (int h = 0; h < CH; ++h) {
                     const int ch = l + h * P;
-                    x[u][h] = (ok && ch < nch) ? __ldg(reinterpret_cast<const float4*>(dOb + (int64_t)iu * dv) + ch)
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                    x[u][h] = (ok && ch < nch) ? ld4(dOb + (int64_t)iu * dv, ch) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
+            // the U = 4 entries summed in f32 (sum4, fixed order), promoted once per value (reading R5)
+            static_assert(U == 4, "the f32 group of the dV gather is 4 entries");
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-#pragma unroll
-                for (int h = 0; h < CH; ++h) {
-                    const double A = (double)Au[u];
-                    acc[h][0] = fma(A, (double)x[u][h].x, acc[h][0]);
-                    acc[h][1] = fma(A, (double)x[u][h].y, acc[h][1]);
-                    acc[h][2] = fma(A, (double)x[u][h].z, acc[h][2]);
-                    acc[h][3] = fma(A, (double)x[u][h].w, acc[h][3]);
-                }
+            for (int h = 0; h < CH; ++h) {
+                acc[h][0] += (double)sum4(Au[0], x[0][h].x, Au[1], x[1][h].x, Au[2], x[2][h].x, Au[3], x[3][h].x);
+                acc[h][1] += (double)sum4(Au[0], x[0][h].y, Au[1], x[1][h].y, Au[2], x[2][h].y, Au[3], x[3][h].y);
+                acc[h][2] += (double)sum4(Au[0], x[0][h].z, Au[1], x[1][h].z, Au[2], x[2][h].z, Au[3], x[3][h].z);
+                acc[h][3] += (double)sum4(Au[0], x[0][h].w, Au[1], x[1][h].w, Au[2], x[2][h].w, Au[3], x[3][h].w);
+            }
         }
         // dK: the lane owning the entry, f64, fixed entry -> lane map
         if (has) {
@@ -455,10 +447,10 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
 }
 
 
-// per-d_k launchers (explicitly instantiated in bwd_dk*.cu)
-template <int DK>
+// per-(d_k, storage type) launchers (explicitly instantiated by bwd_inst.cu's units)
+template <int DK, typename TV>
 void launch_bwd_query_dk(const BwdArgs& a, int P, int nch, int dv, int k, unsigned grid, cudaStream_t st);
-template <int DK>
+template <int DK, typename TV>
 void launch_bwd_key_dk(const KeyArgs& ka, int P, int dv, unsigned grid, cudaStream_t st);
 
 }  // namespace onedf

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "onedf.h"
@@ -45,6 +46,39 @@ template <int DK>
 struct RecW { static constexpr int value = (DK + 1 + 3) / 4 * 4; };
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+
+// ---------------------------------------------------------------- value rows (V, O, dO, dV)
+// Storage type of the d_v-wide rows (onedf_problem.vdtype, reading D26): float,
+// or bfloat16 widened exactly on load and rounded once (RN) from f64 on store.
+// A row is addressed in chunks of 4 values (16 B float / 8 B bf16).
+using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ float4 ld4(const float* p, int64_t c4) {
+    return __ldg(reinterpret_cast<const float4*>(p) + c4);
+}
+__device__ __forceinline__ float4 ld4(const bf16* p, int64_t c4) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p) + c4);
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                       __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+}
+// one value (the column scans)
+__device__ __forceinline__ float ld1(const float* p, int64_t i) { return __ldg(p + i); }
+__device__ __forceinline__ float ld1(const bf16* p, int64_t i) {
+    return __uint_as_float((unsigned)__ldg(reinterpret_cast<const unsigned short*>(p) + i) << 16);
+}
+
+__device__ __forceinline__ void st4(float* p, int64_t c4, double a, double b, double c, double d) {
+    reinterpret_cast<float4*>(p)[c4] = make_float4((float)a, (float)b, (float)c, (float)d);
+}
+__device__ __forceinline__ unsigned bf16_bits(double x) {
+    return (unsigned)__bfloat16_as_ushort(__double2bfloat16(x));     // cvt.rn.bf16.f64: one rounding
+}
+__device__ __forceinline__ void st4(bf16* p, int64_t c4, double a, double b, double c, double d) {
+    reinterpret_cast<uint2*>(p)[c4] = make_uint2(bf16_bits(a) | (bf16_bits(b) << 16), bf16_bits(c) | (bf16_bits(d) << 16));
+}
+__device__ __forceinline__ void st1(float* p, int64_t i, double x) { p[i] = (float)x; }
+__device__ __forceinline__ void st1(bf16* p, int64_t i, double x) { p[i] = __double2bfloat16(x); }
+
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -75,6 +109,17 @@ __device__ __forceinline__ float rank_dist32(const float* q, const float* k) {
         acc = __fadd_rn(acc, __fmul_rn(t, t));
     }
     return acc;
+}
+
+// Sum of 4 f32 products in the fixed order ((a0 b0 + a1 b1) + a2 b2) + a3 b3 with explicit
+// roundings (no contraction choice left to the compiler): the f32 group of the gathers, which the
+// caller adds into an f64 accumulator -- one f32->f64 conversion per 4 products (reading R5).
+__device__ __forceinline__ float sum4(float a0, float b0, float a1, float b1, float a2, float b2, float a3,
+                                      float b3) {
+    float s = __fmul_rn(a0, b0);
+    s = __fmaf_rn(a1, b1, s);
+    s = __fmaf_rn(a2, b2, s);
+    return __fmaf_rn(a3, b3, s);
 }
 
 // f64 squared distance used for the Cauchy weights (exact products of f32 data).
@@ -237,6 +282,11 @@ __device__ __forceinline__ void set_flag(void* ws, int op, unsigned bit) {
 }
 
 }  // namespace onedf
+
+// value storage type of a problem (onedf.h ONEDF_DTYPE_*) as a C++ type TV
+#define ONEDF_DISPATCH_TV(vdtype, ...)                                       \
+    if ((vdtype) == ONEDF_DTYPE_BF16) { using TV = onedf::bf16; __VA_ARGS__; } \
+    else { using TV = float; __VA_ARGS__; }
 
 #define ONEDF_DISPATCH_DK(dk, ...)                        \
     switch (dk) {                                         \

@@ -34,29 +34,9 @@
 //      accumulators; V rows are gathered as float4 bursts (16 lanes per
 //      64-float row), lane groups split the slots and are combined by a fixed
 //      shuffle tree (deterministic).
-#include "common.cuh"
-#include "internal.h"
+#include "fwd_kernels.cuh"
 
 namespace onedf {
-
-constexpr int FWD_WARPS = 8;
-constexpr int FWD_THREADS = FWD_WARPS * 32;
-#ifndef ONEDF_FWD_QPW
-#define ONEDF_FWD_QPW 4
-#endif
-#ifndef ONEDF_FWD_UB
-#define ONEDF_FWD_UB 4
-#endif
-#ifndef ONEDF_FWD_MINB
-#define ONEDF_FWD_MINB 4
-#endif
-constexpr int FWD_QPW = ONEDF_FWD_QPW;              // queries per warp (schedule stretch per CTA = 8*QPW)
-constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 loaded ahead (W = 128 -> one window)
-#ifndef ONEDF_FWD_TBITS
-#define ONEDF_FWD_TBITS 18                          // bisection of T stops at 2^(TBITS-23) relative width
-#endif
-constexpr int FWD_CAP = 256;                        // pass-2 collection capacity per warp
-constexpr unsigned long long KEY_MAX = ~0ull;
 
 void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f) {
     const int64_t BH = p->B * p->H;
@@ -86,654 +66,24 @@ __global__ void build_records_kernel(const float* __restrict__ K, const int32_t*
     for (int v = 0; v < REC / 4; ++v) dst[v] = make_float4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
 }
 
-// ------------------------------------------------------------------ register top-k
-// Merge the 32 pending keys (one per lane, unsorted; KEY_MAX = empty) into the
-// ascending top list top[R] (element e = r*32 + lane), keeping the lowest 32R.
-template <int R>
-__device__ __forceinline__ void merge_pending(unsigned long long (&top)[R], unsigned long long x) {
-    const int lane = lane_id();
-    x = warp_sort32(x);
-    // reversed pending against the last row: min(A ascending, B descending) is bitonic
-    const unsigned long long y = __shfl_sync(FULL, x, 31 - lane);
-    top[R - 1] = umin64(top[R - 1], y);
-    // half-cleaners over KC = 32R elements: register strides, then lane strides
-#pragma unroll
-    for (int rs = R / 2; rs > 0; rs >>= 1) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            if ((r & rs) == 0) {
-                const unsigned long long a = top[r], b = top[r + rs];
-                top[r] = umin64(a, b);
-                top[r + rs] = umax64(a, b);
-            }
-        }
-    }
-#pragma unroll
-    for (int stride = 16; stride > 0; stride >>= 1) {
-        const bool lower = (lane & stride) == 0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const unsigned long long y2 = __shfl_xor_sync(FULL, top[r], stride);
-            top[r] = lower ? umin64(top[r], y2) : umax64(top[r], y2);
-        }
-    }
-}
-
-// The first 32*RS of buf[0..cnt) (KEY_MAX-padded), bitonic-sorted into top[0..RS); top[RS..R) = KEY_MAX.
-template <int RS, int R>
-__device__ __forceinline__ void sort_rows(const unsigned long long* buf, int cnt, unsigned long long (&top)[R]) {
-    const int lane = lane_id();
-    unsigned long long x[RS];
-#pragma unroll
-    for (int r = 0; r < RS; ++r) x[r] = r * 32 + lane < cnt ? buf[r * 32 + lane] : KEY_MAX;
-    if (RS == 1) x[0] = warp_sort32(x[0]);
-    else warp_sort<RS>(x);
-#pragma unroll
-    for (int r = 0; r < R; ++r) top[r] = r < RS ? x[r < RS ? r : 0] : KEY_MAX;
-}
-
-// Element e of the distributed list (e runtime, warp-uniform).
-template <int R>
-__device__ __forceinline__ unsigned long long list_get(const unsigned long long (&top)[R], int e) {
-    unsigned long long v = top[0];
-#pragma unroll
-    for (int r = 1; r < R; ++r) v = (e >> 5) == r ? top[r] : v;
-    return __shfl_sync(FULL, v, e & 31);
-}
-
-#ifdef ONEDF_FWD_STATS
-__device__ unsigned long long g_fwd_stats[8];
-#endif
-
-struct FwdArgs {
-    const float* Q; const float* K; const float* V; const float* eps;
-    const uint64_t* qcode; const uint64_t* scode; const float* recs; const int32_t* qorder;
-    const float* Kbar; const float* Vbar;
-    float* O; int32_t* idx; float* Z;
-    int64_t N, M, total, nq;     // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
-    int k, W, dv, causal, mean_slot, score;
-    Shard sh;
-    void* ws;
-};
-
-// Per-query view of the candidate set C_i (A5): the admissible runs, their
-// windows, and a visitor that streams every candidate of C_i through a
-// callback in fixed (run, rank) order, FWD_UB batches of 32 at a time.
-template <int DK>
-struct CandSet {
-    const float* q;
-    uint64_t qc;
-    const uint64_t* scode;       // this (b,h) row
-    const float4* recs4;         // this (b,h) row of sorted key records
-    int64_t N, M, nruns;
-    int W, causal;
-
-    // lane c of the warp: window (base, w) of run c0 + c (lower_bound, D2/D3)
-    __device__ __forceinline__ void window(int64_t c, int64_t& base, int& w) const {
-        base = 0;
-        w = 0;
-        if (c < nruns) {
-            const int64_t s0 = causal ? c * M : 0;
-            const int64_t len = causal ? min64(M, N - s0) : N;
-            int64_t lo = 0, hi = len;
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (__ldg(scode + s0 + mid) < qc) lo = mid + 1; else hi = mid;
-            }
-            const int64_t ww = min64(W, len);
-            int64_t st = lo - W / 2;
-            st = st < 0 ? 0 : st;
-            st = st > len - ww ? len - ww : st;
-            base = s0 + st;
-            w = (int)ww;
-        }
-    }
-
-    // One stretch of FWD_UB batches of 32 window entries starting at rank r0.
-    template <bool FULL, class F>
-    __device__ __forceinline__ bool stretch(const float4* wp, int r0, int ww, F&& f) const {
-        constexpr int REC = RecW<DK>::value;
-        const int lane = lane_id();
-        float D[FWD_UB];
-        int jj[FWD_UB];
-        bool ok[FWD_UB];
-#pragma unroll
-        for (int u = 0; u < FWD_UB; ++u) {
-            ok[u] = FULL || r0 + 32 * u + lane < ww;
-            D[u] = 0.f;
-            jj[u] = 0;
-            if (ok[u]) {
-                float rv[REC];
-#pragma unroll
-                for (int v = 0; v < REC / 4; ++v) {
-                    const float4 t4 = __ldg(wp + (r0 + 32 * u) * (REC / 4) + v);
-                    rv[4 * v] = t4.x; rv[4 * v + 1] = t4.y; rv[4 * v + 2] = t4.z; rv[4 * v + 3] = t4.w;
-                }
-                D[u] = rank_dist32<DK>(q, rv);
-                jj[u] = __float_as_int(rv[DK]);
-            }
-        }
-        return f(D, jj, ok, r0, ww);
-    }
-
-    // f(D[FWD_UB], j[FWD_UB], valid[FWD_UB]) per stretch; returns false to stop.
-    // (base0, w0) are the lane-parallel windows of runs 0..31, computed once.
-    template <class F>
-    __device__ __forceinline__ bool visit(int64_t base0, int w0, F&& f) const {
-        constexpr int REC = RecW<DK>::value;
-        const int lane = lane_id();
-        for (int64_t c0 = 0; c0 < nruns; c0 += 32) {
-            int64_t base = base0;
-            int w = w0;
-            if (c0 > 0) window(c0 + lane, base, w);
-            const int nc = (int)min64(32, nruns - c0);
-            for (int cc = 0; cc < nc; ++cc) {
-                const int b = (int)__shfl_sync(FULL, base, cc);
-                const int ww = __shfl_sync(FULL, w, cc);
-                const float4* wp = recs4 + (b + lane) * (REC / 4);
-                if (ww % (32 * FWD_UB) == 0) {
-                    // full stretches (the common case: W = 128 = 4 x 32): no per-lane bounds checks
-                    for (int r0 = 0; r0 < ww; r0 += 32 * FWD_UB) {
-                        if (!stretch<true>(wp, r0, ww, f)) return false;
-                    }
-                } else {
-                    for (int r0 = 0; r0 < ww; r0 += 32 * FWD_UB) {
-                        if (!stretch<false>(wp, r0, ww, f)) return false;
-                    }
-                }
-            }
-        }
-        return true;
-    }
-};
-
-__device__ __forceinline__ unsigned long long make_key(float D, int j) {
-    return ((unsigned long long)__float_as_uint(D) << 32) | (unsigned)j;
-}
-
-// Pass 1 list length per lane: the union of the per-lane lists (32 L values)
-// must hold at least k of them; L = 2 * ceil(k/32) gives 2k.
-template <int R>
-struct PassOne { static constexpr int L = 2 * R; };
-
-// A7 for one query: weights (f64) of the selected keys jr[] (slot e = r*32 + lane,
-// -1 = empty) and the mean slot, the normaliser Z, and the value gather o.
-template <int DK, int R>
-__device__ __forceinline__ void attend_row(const FwdArgs& a, int64_t bh, int64_t i, int64_t gq, const float* q,
-                                           const int (&jr)[R], int nsel, double ed) {
-    const int lane = lane_id();
-    const int64_t N = a.N;
-    // ---------------- A7: weights (f64): Cauchy Eq. 5, or a score variant (D24)
-    const int sc = a.score;
-    double Sr[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        Sr[r] = 0.0;
-        if (jr[r] >= 0) {
-            float kj[DK];
-#pragma unroll
-            for (int d = 0; d < DK; ++d) kj[d] = __ldg(a.K + (bh * N + jr[r]) * DK + d);
-            Sr[r] = score_raw<DK>(sc, q, kj, ed);
-        }
-    }
-    double Smu = 0.0;
-    const int64_t mrow = a.causal ? i : 0;
-    if (a.mean_slot) {
-        float kb[DK];
-#pragma unroll
-        for (int d = 0; d < DK; ++d) kb[d] = __ldg(a.Kbar + (bh * (a.causal ? N : 1) + mrow) * DK + d);
-        Smu = score_raw<DK>(sc, q, kb, ed);
-    }
-    double xmax = 0.0;
-    if (score_is_exp(sc)) {
-        // softmax scores: shift by the largest logit (fixed-order warp max), S = exp(x - xmax)
-        double m = -INFINITY;
-#pragma unroll
-        for (int r = 0; r < R; ++r) m = jr[r] >= 0 ? fmax(m, Sr[r]) : m;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(FULL, m, o));
-        if (a.mean_slot) m = fmax(m, Smu);
-        xmax = m;
-#pragma unroll
-        for (int r = 0; r < R; ++r) Sr[r] = jr[r] >= 0 ? exp(Sr[r] - xmax) : 0.0;
-        if (a.mean_slot) Smu = exp(Smu - xmax);
-    }
-    double zpart = 0.0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) zpart += Sr[r];
-    double Zi = warp_sum(zpart);
-    if (a.mean_slot) Zi += Smu;
-    const double invZ = Zi > 0.0 ? 1.0 / Zi : 0.0;
-
-    // ---------------- A7: value gather, float4 chunks, lane groups over slots
-    const int nch = a.dv / 4;
-    int P = 1;
-    while (P < nch && P < 32) P <<= 1;
-    const int G = 32 / P;                 // rows per step (1 when nch >= 32)
-    const int grp = lane / P, ch_l = lane % P;
-    const float* Vb = a.V + bh * N * (int64_t)a.dv;
-    float* orow = a.O + gq * (int64_t)a.dv;
-    const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)a.dv;
-    const double Amu = Smu * invZ;
-    for (int ch0 = 0; ch0 < nch; ch0 += P) {
-        const int ch = ch0 + ch_l;
-        const bool act = ch < nch;
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            if (r * 32 >= nsel) break;
-            for (int t0 = 0; t0 < 32 && r * 32 + t0 < nsel; t0 += 4 * G) {
-                float4 v4[4];
-                double A4[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int src = (t0 + u * G + grp) & 31;
-                    const int j = __shfl_sync(FULL, jr[r], src);
-                    A4[u] = __shfl_sync(FULL, Sr[r], src) * invZ;
-                    const bool ok = act && t0 + u * G + grp < 32 && r * 32 + t0 + u * G + grp < nsel;
-                    v4[u] = ok ? __ldg(reinterpret_cast<const float4*>(Vb + (int64_t)j * a.dv) + ch)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (!ok) A4[u] = 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    acc0 = fma(A4[u], (double)v4[u].x, acc0);
-                    acc1 = fma(A4[u], (double)v4[u].y, acc1);
-                    acc2 = fma(A4[u], (double)v4[u].z, acc2);
-                    acc3 = fma(A4[u], (double)v4[u].w, acc3);
-                }
-            }
-        }
-        for (int o = P; o < 32; o <<= 1) {
-            acc0 += __shfl_xor_sync(FULL, acc0, o);
-            acc1 += __shfl_xor_sync(FULL, acc1, o);
-            acc2 += __shfl_xor_sync(FULL, acc2, o);
-            acc3 += __shfl_xor_sync(FULL, acc3, o);
-        }
-        if (grp == 0 && act) {
-            if (a.mean_slot) {
-                const float4 vb = __ldg(reinterpret_cast<const float4*>(vbar) + ch);
-                acc0 = fma(Amu, (double)vb.x, acc0);
-                acc1 = fma(Amu, (double)vb.y, acc1);
-                acc2 = fma(Amu, (double)vb.z, acc2);
-                acc3 = fma(Amu, (double)vb.w, acc3);
-            }
-            reinterpret_cast<float4*>(orow)[ch] =
-                make_float4((float)acc0, (float)acc1, (float)acc2, (float)acc3);
-        }
-    }
-    if (lane == 0) a.Z[gq] = (float)(score_is_exp(sc) ? (Zi > 0.0 ? xmax + log(Zi) : 0.0) : Zi);
-}
-
-template <int DK, int R>
-__global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_kernel(const FwdArgs a) {
-    constexpr int L = PassOne<R>::L;
-    __shared__ __align__(16) unsigned long long s_buf[FWD_WARPS][FWD_CAP];
-    __shared__ int s_cnt[FWD_WARPS];
-    const int warp = threadIdx.x / 32, lane = lane_id();
-    unsigned long long* buf = s_buf[warp];
-    const float e = __ldg(a.eps);
-    if (a.score == SC_CAUCHY && blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e)))
-        set_flag(a.ws, ONEDF_OP_FWD, FLAG_BAD_EPS);
-    const double ed = (double)e;
-    const int64_t N = a.N;
-    const int k = a.k;
-    constexpr int REC = RecW<DK>::value;
-
-    for (int u = 0; u < FWD_QPW; ++u) {
-        const int64_t slot = ((int64_t)blockIdx.x * FWD_QPW + u) * FWD_WARPS + warp;
-        if (slot >= a.total) break;
-        const int64_t bh = slot / a.nq;
-        int64_t pos;
-        if (!a.sh.slot_pos(slot - bh * a.nq, N, pos)) continue;     // sharded: padding of a short last chunk
-        const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + bh * N + pos) : pos;
-        const int64_t gq = bh * N + i;
-
-        float q[DK];
-#pragma unroll
-        for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
-        CandSet<DK> cs;
-        cs.q = q;
-        cs.qc = __ldg(a.qcode + gq);
-        cs.scode = a.scode + bh * N;
-        cs.recs4 = reinterpret_cast<const float4*>(a.recs + bh * N * REC);
-        cs.N = N; cs.M = a.M; cs.W = a.W; cs.causal = a.causal;
-        cs.nruns = a.causal ? i / a.M : 1;
-        int64_t base0;
-        int w0;
-        cs.window(lane, base0, w0);
-
-        // ---------------- A6 pass 1: per-lane L smallest D (f32 min/max chain).
-        // The k-th smallest of the union of these lists is an upper bound T on
-        // the k-th smallest D of C_i (k distinct candidates lie at or below it).
-        float lst[L];
-#pragma unroll
-        for (int t = 0; t < L; ++t) lst[t] = INFINITY;
-        cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&)[FWD_UB], const bool (&ok)[FWD_UB], int, int) {
-#pragma unroll
-            for (int uu = 0; uu < FWD_UB; ++uu) {
-                float x = ok[uu] ? D[uu] : INFINITY;
-#pragma unroll
-                for (int t = 0; t < L; ++t) {
-                    const float lo = fminf(lst[t], x);
-                    x = fmaxf(lst[t], x);
-                    lst[t] = lo;
-                }
-            }
-            return true;
-        });
-        // T: a bit pattern with #{values <= T} >= k (non-negative floats order as
-        // their bits).  Bisection between the smallest list head and the largest
-        // list tail, stopped at 2^(TBITS-23) relative width: any such T is a valid
-        // bound, a slightly larger one only admits a few more keys in pass 2.
-        unsigned tb;
-        {
-            float fmn = lst[0], fmx = lst[L - 1];
-            unsigned finite = 0;
-#pragma unroll
-            for (int t = 0; t < L; ++t) finite += lst[t] < INFINITY;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) fmn = fminf(fmn, __shfl_xor_sync(FULL, fmn, o));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
-            if (__reduce_add_sync(FULL, finite) < (unsigned)k) {
-                tb = 0x7f800000u;                          // fewer than k candidates: admit all
-            } else {
-                unsigned lo = __float_as_uint(fmn), hi = __float_as_uint(fmx);   // count(<= hi) >= k
-#pragma unroll 1
-                while (hi - lo > (1u << ONEDF_FWD_TBITS)) {   // stop at 2^(TBITS-23) relative resolution
-                    const unsigned mid = lo + ((hi - lo) >> 1);
-                    unsigned c = 0;
-#pragma unroll
-                    for (int t = 0; t < L; ++t) c += __float_as_uint(lst[t]) <= mid;
-                    if (__reduce_add_sync(FULL, c) >= (unsigned)k) hi = mid; else lo = mid + 1;
-                }
-                tb = hi;
-            }
-        }
-
-        // ---------------- A6 pass 2: collect every candidate with D <= T (order is
-        // irrelevant: the final order comes from ranking the unique keys)
-        int cnt = 0;
-        if (lane == 0) s_cnt[warp] = 0;
-        __syncwarp();
-        cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB], const bool (&ok)[FWD_UB], int,
-                                int) {
-#pragma unroll
-            for (int uu = 0; uu < FWD_UB; ++uu) {
-                if (ok[uu] && __float_as_uint(D[uu]) <= tb) {
-                    const int pos = atomicAdd(&s_cnt[warp], 1);
-                    if (pos < FWD_CAP) buf[pos] = make_key(D[uu], jj[uu]);
-                }
-            }
-            return true;
-        });
-        __syncwarp();
-        cnt = s_cnt[warp];
-        const bool fits = cnt <= FWD_CAP;
-#ifdef ONEDF_FWD_STATS
-        if (lane == 0) {
-            atomicAdd(&g_fwd_stats[0], 1ull);
-            atomicAdd(&g_fwd_stats[1], (unsigned long long)cnt);
-            atomicAdd(&g_fwd_stats[2], (unsigned long long)cnt * cnt);
-            atomicAdd(&g_fwd_stats[3], fits ? 0ull : 1ull);
-        }
-#endif
-        __syncwarp();
-        unsigned long long top[R];
-        if (fits) {
-            // ---------------- exact order of the collected keys: the first rows (up to R) are
-            // bitonic-sorted together into the register top list, every further 32-key row is
-            // merged in (shuffle bitonic sort of the row + min-merge + half-cleaners)
-            const int rows = (cnt + 31) / 32;
-            int m0;
-            if (rows <= 1 || R == 1) { sort_rows<1, R>(buf, cnt, top); m0 = 1; }
-            else if (rows <= 2 || R == 2) { sort_rows<(R >= 2 ? 2 : 1), R>(buf, cnt, top); m0 = 2; }
-            else if (rows <= 4 || R == 4) { sort_rows<(R >= 4 ? 4 : 1), R>(buf, cnt, top); m0 = 4; }
-            else { sort_rows<(R >= 8 ? 8 : 1), R>(buf, cnt, top); m0 = 8; }
-            for (int m = m0; m * 32 < cnt; ++m)
-                merge_pending<R>(top, m * 32 + lane < cnt ? buf[m * 32 + lane] : KEY_MAX);
-        } else {
-            // ---------------- rare: too many keys at or below T (e.g. many equal
-            // distances) -- streaming selection with shuffle-bitonic merges,
-            // starting from the same bound
-#pragma unroll
-            for (int r = 0; r < R; ++r) top[r] = KEY_MAX;
-            unsigned long long thresh = tb >= 0x7f800000u ? KEY_MAX : ((unsigned long long)(tb + 1u) << 32);
-            unsigned long long* pend = buf;
-            int pc = 0;
-            cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB], const bool (&ok)[FWD_UB], int,
-                                    int) {
-#pragma unroll
-                for (int uu = 0; uu < FWD_UB; ++uu) {
-                    const unsigned long long key = ok[uu] ? make_key(D[uu], jj[uu]) : KEY_MAX;
-                    bool pass = key < thresh;
-                    unsigned m = __ballot_sync(FULL, pass);
-                    if (m == 0) continue;
-                    int n = __popc(m);
-                    if (pc + n > 32) {
-                        __syncwarp();
-                        merge_pending<R>(top, lane < pc ? pend[lane] : KEY_MAX);
-                        thresh = umin64(thresh, list_get<R>(top, k - 1));
-                        pc = 0;
-                        pass = key < thresh;
-                        m = __ballot_sync(FULL, pass);
-                        n = __popc(m);
-                    }
-                    if (pass) pend[pc + __popc(m & lanemask_lt())] = key;
-                    pc += n;
-                    __syncwarp();
-                }
-                return true;
-            });
-            if (pc > 0) {
-                __syncwarp();
-                merge_pending<R>(top, lane < pc ? pend[lane] : KEY_MAX);
-            }
-        }
-        __syncwarp();   // buf/stop are rewritten by the next query
-
-        // ---------------- outputs: idx row (slot e = r*32 + lane), valid count
-        int32_t* idx_row = a.idx + gq * k;
-        int jr[R];
-        int nsel = 0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int e2 = r * 32 + lane;
-            const bool valid = e2 < k && top[r] != KEY_MAX;
-            jr[r] = valid ? (int)(unsigned)(top[r] & 0xffffffffull) : -1;
-            if (e2 < k) idx_row[e2] = jr[r];
-            nsel += __popc(__ballot_sync(FULL, valid));
-        }
-
-        attend_row<DK, R>(a, bh, i, gq, q, jr, nsel, ed);
-
-    }
-}
-
-// ------------------------------------------------------------------ selection variant (D25)
-// SPEC's query_topk: the same per-run windows, candidates ordered by
-// (|scode - qcode| as u64, j) -- NEXT-2's code-distance merge.  One warp per
-// query: (1) per-lane lists of the 2R smallest u64 distances bound the k-th
-// distance T (bisection over the union of the lists); (2) every candidate with
-// distance <= T is appended to shared memory and ranked by (distance, j) (the
-// pairs are unique); more than CODE_CAP such candidates (repeated codes) fall
-// back to k rounds of a warp-wide minimum above the last pair.  Then the same
-// A7 as the Euclidean path (attend_row).
-constexpr int CODE_CAP = 256;
-
-__device__ __forceinline__ bool pair_lt(unsigned long long d0, int j0, unsigned long long d1, int j1) {
-    return d0 < d1 || (d0 == d1 && j0 < j1);
-}
-
-template <int DK, int R>
-__global__ void __launch_bounds__(FWD_THREADS) code_select_attn_kernel(const FwdArgs a) {
-    constexpr int L = 2 * R;
-    constexpr int REC = RecW<DK>::value;
-    __shared__ unsigned long long s_d[FWD_WARPS][CODE_CAP];
-    __shared__ int s_j[FWD_WARPS][CODE_CAP];
-    __shared__ int s_cnt[FWD_WARPS];
-    const int warp = threadIdx.x / 32, lane = lane_id();
-    const float e = __ldg(a.eps);
-    if (a.score == SC_CAUCHY && blockIdx.x == 0 && threadIdx.x == 0 && !(e > 0.f && isfinite(e)))
-        set_flag(a.ws, ONEDF_OP_FWD, FLAG_BAD_EPS);
-    const double ed = (double)e;
-    const int64_t N = a.N;
-    const int k = a.k;
-    for (int u = 0; u < FWD_QPW; ++u) {
-        const int64_t slot = ((int64_t)blockIdx.x * FWD_QPW + u) * FWD_WARPS + warp;
-        if (slot >= a.total) break;
-        const int64_t bh = slot / a.nq;
-        int64_t pos;
-        if (!a.sh.slot_pos(slot - bh * a.nq, N, pos)) continue;
-        const int64_t i = a.qorder ? (int64_t)__ldg(a.qorder + bh * N + pos) : pos;
-        const int64_t gq = bh * N + i;
-        float q[DK];
-#pragma unroll
-        for (int d = 0; d < DK; ++d) q[d] = __ldg(a.Q + gq * DK + d);
-        CandSet<DK> cs;
-        cs.q = q;
-        cs.qc = __ldg(a.qcode + gq);
-        cs.scode = a.scode + bh * N;
-        cs.recs4 = reinterpret_cast<const float4*>(a.recs + bh * N * REC);
-        cs.N = N; cs.M = a.M; cs.W = a.W; cs.causal = a.causal;
-        cs.nruns = a.causal ? i / a.M : 1;
-        const uint64_t qc = cs.qc;
-        const float* recs = a.recs + bh * N * REC;
-        // stream (distance, j, valid) of every candidate, 32 at a time, fixed (run, rank) order
-        auto visit = [&](auto&& f) {
-            for (int64_t c0 = 0; c0 < cs.nruns; c0 += 32) {
-                int64_t base; int w;
-                cs.window(c0 + lane, base, w);
-                const int nc = (int)min64(32, cs.nruns - c0);
-                for (int cc = 0; cc < nc; ++cc) {
-                    const int64_t b = __shfl_sync(FULL, base, cc);
-                    const int ww = __shfl_sync(FULL, w, cc);
-                    for (int r0 = 0; r0 < ww; r0 += 32) {
-                        const bool ok = r0 + lane < ww;
-                        unsigned long long d = ~0ull;
-                        int j = -1;
-                        if (ok) {
-                            const uint64_t kc = __ldg(cs.scode + b + r0 + lane);
-                            d = kc > qc ? kc - qc : qc - kc;
-                            j = __float_as_int(__ldg(recs + (b + r0 + lane) * REC + DK));
-                        }
-                        f(d, j, ok);
-                    }
-                }
-            }
-        };
-        // (1) per-lane L smallest distances -> bound T with #{d <= T} >= k
-        unsigned long long lst[L];
-#pragma unroll
-        for (int t = 0; t < L; ++t) lst[t] = ~0ull;
-        visit([&](unsigned long long d, int, bool ok) {
-            unsigned long long x = ok ? d : ~0ull;
-#pragma unroll
-            for (int t = 0; t < L; ++t) {
-                const unsigned long long lo = umin64(lst[t], x);
-                x = umax64(lst[t], x);
-                lst[t] = lo;
-            }
-        });
-        unsigned long long T;
-        {
-            unsigned finite = 0;
-#pragma unroll
-            for (int t = 0; t < L; ++t) finite += lst[t] != ~0ull;
-            if (__reduce_add_sync(FULL, finite) < (unsigned)k) {
-                T = ~0ull;                                    // fewer than k candidates (or a +inf-like distance)
-            } else {
-                unsigned long long lo = lst[0], hi = 0;
-#pragma unroll
-                for (int t = 0; t < L; ++t) hi = lst[t] != ~0ull ? umax64(hi, lst[t]) : hi;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    lo = umin64(lo, __shfl_xor_sync(FULL, lo, o));
-                    hi = umax64(hi, __shfl_xor_sync(FULL, hi, o));
-                }
-                while (lo < hi) {                             // smallest T with count(<= T) >= k
-                    const unsigned long long mid = lo + ((hi - lo) >> 1);
-                    unsigned c = 0;
-#pragma unroll
-                    for (int t = 0; t < L; ++t) c += lst[t] <= mid;
-                    if (__reduce_add_sync(FULL, c) >= (unsigned)k) hi = mid; else lo = mid + 1;
-                }
-                T = hi;
-            }
-        }
-        // (2) collect every candidate with d <= T
-        if (lane == 0) s_cnt[warp] = 0;
-        __syncwarp();
-        unsigned long long* sd = s_d[warp];
-        int* sj = s_j[warp];
-        visit([&](unsigned long long d, int j, bool ok) {
-            if (ok && d <= T) {
-                const int p2 = atomicAdd(&s_cnt[warp], 1);
-                if (p2 < CODE_CAP) { sd[p2] = d; sj[p2] = j; }
-            }
-        });
-        __syncwarp();
-        const int cnt = s_cnt[warp];
-        int32_t* idx_row = a.idx + gq * k;
-        if (cnt <= CODE_CAP) {
-            for (int t = lane; t < k; t += 32) idx_row[t] = -1;
-            __syncwarp();
-            for (int m = lane; m < cnt; m += 32) {
-                const unsigned long long dm = sd[m];
-                const int jm = sj[m];
-                int rank = 0;
-                for (int x = 0; x < cnt; ++x) rank += pair_lt(sd[x], sj[x], dm, jm);
-                if (rank < k) idx_row[rank] = jm;
-            }
-        } else {
-            // many equal distances: k rounds of "smallest pair above the last one"
-            unsigned long long ld = 0;
-            int lj = -1;
-            bool first = true;
-            for (int t = 0; t < k; ++t) {
-                unsigned long long bd = ~0ull;
-                int bj = 0x7fffffff;
-                visit([&](unsigned long long d, int j, bool ok) {
-                    if (ok && (first || pair_lt(ld, lj, d, j)) && pair_lt(d, j, bd, bj)) { bd = d; bj = j; }
-                });
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const unsigned long long od = __shfl_xor_sync(FULL, bd, o);
-                    const int oj = __shfl_xor_sync(FULL, bj, o);
-                    if (pair_lt(od, oj, bd, bj)) { bd = od; bj = oj; }
-                }
-                if (lane == 0) idx_row[t] = bj == 0x7fffffff ? -1 : bj;
-                ld = bd; lj = bj; first = false;
-            }
-        }
-        __syncwarp();
-        int jr[R];
-        int nsel = 0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int e2 = r * 32 + lane;
-            jr[r] = e2 < k ? idx_row[e2] : -1;
-            nsel += __popc(__ballot_sync(FULL, jr[r] >= 0));
-        }
-        attend_row<DK, R>(a, bh, i, gq, q, jr, nsel, ed);
-        __syncwarp();   // s_d/s_j/s_cnt are rewritten by the next query
-    }
-}
-
-cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                       const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
-                       float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st, const Trace& tr) {
+cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
+                       const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
+                       void* O, int32_t* idx, float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st,
+                       const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
     ONEDF_DISPATCH_DK(p->d_k, {
         build_records_kernel<DK><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(K, perm, f->recs, N, total);
     });
-    cudaError_t e = launch_query_order(p, qcode, f->qorder, f->scr, st);
-    if (e != cudaSuccess) return e;
+    if (!qorder) {
+        // no schedule from the caller: sort the query codes here (onedf_sort of qcode)
+        const cudaError_t e = launch_query_order(p, qcode, f->qorder, f->scr, st);
+        if (e != cudaSuccess) return e;
+        qorder = f->qorder;
+    }
     tr.mark(1, st);
     FwdArgs a;
     a.Q = Q; a.K = K; a.V = V; a.eps = eps; a.qcode = qcode; a.scode = scode; a.recs = f->recs;
-    a.qorder = f->qorder;
+    a.qorder = qorder;
     a.Kbar = m->Kbar; a.Vbar = m->Vbar; a.O = O; a.idx = idx; a.Z = Z;
     a.sh = make_shard(p);
     a.nq = a.sh.slots(N);
@@ -743,30 +93,15 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
     a.ws = ws;
     const int64_t per_cta = (int64_t)FWD_WARPS * FWD_QPW;
     const unsigned grid = (unsigned)((a.total + per_cta - 1) / per_cta);
-#define ONEDF_FWD_R(RV)                                                                                  \
-    ONEDF_DISPATCH_DK(p->d_k, {                                                                          \
-        if (!grid) {}                                                                                    \
-        else if (p->select) code_select_attn_kernel<DK, RV><<<grid, FWD_THREADS, 0, st>>>(a);           \
-        else topk_attn_fwd_kernel<DK, RV><<<grid, FWD_THREADS, 0, st>>>(a);                             \
-    })
-    if (p->k <= 32) { ONEDF_FWD_R(1) }
-    else if (p->k <= 64) { ONEDF_FWD_R(2) }
-    else if (p->k <= 128) { ONEDF_FWD_R(4) }
-    else { ONEDF_FWD_R(8) }
-#undef ONEDF_FWD_R
+    ONEDF_DISPATCH_TV(p->vdtype, {
+        if (p->k <= 32) launch_fwd_tv<TV, 1>(a, p, grid, st);
+        else if (p->k <= 64) launch_fwd_tv<TV, 2>(a, p, grid, st);
+        else if (p->k <= 128) launch_fwd_tv<TV, 4>(a, p, grid, st);
+        else launch_fwd_tv<TV, 8>(a, p, grid, st);
+    });
     tr.mark(2, st);
     return cudaGetLastError();
 }
 
 }  // namespace onedf
 
-#ifdef ONEDF_FWD_STATS
-// tools only (variant builds): [queries, sum cnt, sum cnt^2, fallbacks], then reset
-extern "C" int onedf_debug_fwd_stats(unsigned long long* out) {
-    cudaDeviceSynchronize();
-    cudaMemcpyFromSymbol(out, onedf::g_fwd_stats, 8 * sizeof(unsigned long long));
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    cudaMemcpyToSymbol(onedf::g_fwd_stats, z, sizeof(z));
-    return 0;
-}
-#endif

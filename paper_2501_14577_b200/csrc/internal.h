@@ -55,16 +55,29 @@ cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, in
 
 
 // csr.cu -- A9 key-major CSR of the selected (query, slot) records
+// Segments longer than this are ordered by csr_long_order_kernel (a bitmap over query positions);
+// shorter ones by the key side itself (register bitonic sort of (i << 8 | position) keys).
+constexpr int KEY_REG_SEG = 256;
+constexpr int KEY_POS_BITS = 8;       // the key side's u32 sort key (i << 8 | position) needs N < 2^24
+__host__ __device__ inline bool csr_long_segment(int64_t len, int64_t N) {
+    return len > KEY_REG_SEG || N >= (1ll << (32 - KEY_POS_BITS));
+}
+
 struct CsrBufs {
     int32_t* cursor;    // [BH][N]    in-degree counts -> insertion cursors
     int32_t* offsets;   // [BH][N+1]  segment of key j = records [off[j], off[j+1])
-    int4* rec;          // [BH][N*k]  record {i, A bits, w bits, 0} of each selected (query, slot)
-    int32_t* order;     // [BH][N*k]  ascending-i order of segments longer than the on-chip limit
+    int32_t* rec_i;     // [BH][N*k]  query position i of each selected (query, slot) record   (SoA:
+    float2* rec_aw;     // [BH][N*k]  its (A_ij, w_ij)                                          12 B/record)
+    int32_t* order;     // [BH][N*k]  ascending-i order of the long segments (csr_long_segment)
+    int32_t* nlong;     // [1]        number of long segments
+    int2* longseg;      // [BH*N]     their (bh, j), in no particular order (each is ordered independently)
 };
 void csr_carve(const onedf_problem* p, Carver* c, CsrBufs* t);
 // qorder: the query schedule (nullable -> natural order); only its grouping of similar queries matters
 cudaError_t launch_csr_count(const onedf_problem* p, const int32_t* idx, const int32_t* qorder, CsrBufs* t,
                              cudaStream_t st);
+// after the query side has appended every record: ascending-i order of each long segment
+cudaError_t launch_csr_long_order(const onedf_problem* p, CsrBufs* t, cudaStream_t st);
 
 // mean.cu
 struct MeanBufs {
@@ -73,11 +86,14 @@ struct MeanBufs {
     double* part;       // scan partials
 };
 void mean_carve(const onedf_problem* p, Carver* c, MeanBufs* m);
-cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const float* V, MeanBufs* m,
+cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const void* V, MeanBufs* m,
                                 cudaStream_t st);
-// A11: dK_t += sum_{i>=t} wmu_i (q_i - Kbar_i)/(i+1), dV_t += sum_{i>=t} Amu_i dO_i/(i+1) (causal; 1/N all i otherwise)
-cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const float* dO, const float* muco,
-                                  MeanBufs* m, float* dK, float* dV, cudaStream_t st);
+// A11: dK_t += sum_{i>=t} wmu_i (q_i - Kbar_i)/(i+1), dV_t = dV32_t + sum_{i>=t} Amu_i dO_i/(i+1) (causal; 1/N
+// all i otherwise); dV32 is the key side's f32 result (== dV for float storage, in place)
+cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const void* dO, const float* muco,
+                                  MeanBufs* m, float* dK, const float* dV32, void* dV, cudaStream_t st);
+// dst = bf16(src), n values (n % 4 == 0)
+cudaError_t launch_round_rows(const float* src, bf16* dst, int64_t n, cudaStream_t st);
 
 // fwd.cu
 struct FwdBufs {
@@ -86,9 +102,11 @@ struct FwdBufs {
     SortScratch scr;    // for the query-order sort of long runs
 };
 void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f);
-cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                       const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, float* O, int32_t* idx,
-                       float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st, const Trace& tr);
+// qorder: the caller's query schedule (nullable -> sorted here from qcode)
+cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
+                       const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
+                       void* O, int32_t* idx, float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st,
+                       const Trace& tr);
 
 // bwd.cu
 constexpr int EPS_PARTS = 1024;   // fixed first-level split of the d_eps reduction
@@ -96,14 +114,25 @@ struct BwdBufs {
     float2* muco;       // [BH][N]    (A_mu, w_mu)
     double* eps_q;      // [BH][N]    per-query d_eps contribution
     double* eps_part;   // [EPS_PARTS]
-    int32_t* qorder;    // [BH][N]    query schedule (when qcode is given)
+    int32_t* qorder;    // [BH][N]    query schedule (when only qcode is given)
+    float* dV32;        // [BH][N][d_v] key-side f32 dV of a BF16 problem (rounded once at the end), else null
     SortScratch scr;    // for the query-order sort of long runs
 };
 void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b);
-cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const float* V, const float* eps,
-                       const float* O, const float* dO, const int32_t* idx, const float* Z, const uint64_t* qcode,
-                       const int32_t* perm, float* dQ, float* dK, float* dV, double* d_eps, const MeanBufs* m,
+cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
+                       const void* dO, const int32_t* idx, const uint64_t* qcode, const int32_t* qorder,
+                       const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, const MeanBufs* m,
                        BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr);
+
+// proj.cu (NEXT-4 projections f_q, f_k and eps = sigma(theta))
+size_t project_ws_bytes(const onedf_problem* p, int d_model, Carver* c);
+cudaError_t launch_project(const onedf_problem* p, int d_model, const float* X, const float* Wq, const float* Wk,
+                           const float* bq, const float* bk, const float* theta, float* Q, float* K, float* eps,
+                           void* ws, cudaStream_t st);
+cudaError_t launch_project_bwd(const onedf_problem* p, int d_model, const float* X, const float* Wq, const float* Wk,
+                               const float* theta, const float* dQ, const float* dK, const double* d_eps, float* dX,
+                               float* dWq, float* dWk, float* dbq, float* dbk, float* dtheta, void* ws,
+                               cudaStream_t st);
 
 // workload.cu (NEXT-3 locality workload)
 cudaError_t launch_code_knn(const onedf_problem* p, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,

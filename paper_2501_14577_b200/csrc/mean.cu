@@ -46,25 +46,31 @@ static int pow2_at_least(int c) {
 //   MODE 1 (A11, K columns): w_mu,i (q_i[c] - Kbar_i[c]) * s_i
 //   MODE 2 (A11, V columns): A_mu,i dO_i[c] * s_i        s_i = 1/(i+1) causal, 1 otherwise
 struct ScanSrc {
-    const float* X;       // MODE 0: K or V; MODE 1: Q; MODE 2: dO
+    const void* X;        // MODE 0: K or V; MODE 1: Q; MODE 2: dO -- element type TX of the kernel
     const float* Kbar;    // MODE 1
     const float2* muco;   // MODE 1, 2
     int C, causal;
     double kt = 1.0;      // MODE 1: w (q - kt Kbar); 0 for the DOT score (dKbar = w q)
 };
 
+// X[e] widened to f64; TX = float, or bf16 for the value rows of a BF16 problem (reading D26)
+template <typename TX>
+__device__ __forceinline__ double xval(const ScanSrc& s, int64_t e) {
+    return (double)ld1(static_cast<const TX*>(s.X), e);
+}
+
 // inv = 1/(i+1) for the causal scans (A11's weights), from the tile's table; 1 otherwise
-template <int MODE>
+template <int MODE, typename TX>
 __device__ __forceinline__ double scan_value(const ScanSrc& s, int64_t bh, int64_t N, int64_t i, int c, double inv) {
     const int64_t row = bh * N + i;
-    if (MODE == 0) return (double)__ldg(s.X + row * s.C + c);
+    if (MODE == 0) return xval<TX>(s, row * s.C + c);
     const float2 mc = __ldg(s.muco + row);
     double y;
     if (MODE == 1) {
         const float kb = __ldg(s.Kbar + (bh * (s.causal ? N : 1) + (s.causal ? i : 0)) * s.C + c);
-        y = (double)mc.y * ((double)__ldg(s.X + row * s.C + c) - s.kt * (double)kb);
+        y = (double)mc.y * (xval<TX>(s, row * s.C + c) - s.kt * (double)kb);
     } else {
-        y = (double)mc.x * (double)__ldg(s.X + row * s.C + c);
+        y = (double)mc.x * xval<TX>(s, row * s.C + c);
     }
     return s.causal ? y * inv : y;
 }
@@ -77,7 +83,7 @@ __device__ __forceinline__ void fill_inv(double* s_inv, int64_t tile) {
 }
 
 // sum of the thread's rows [r0, r1), loads batched SCAN_UNROLL at a time, fixed order
-template <int MODE>
+template <int MODE, typename TX>
 __device__ __forceinline__ double rows_sum(const ScanSrc& s, int64_t bh, int64_t N, int64_t r0, int64_t r1, int c,
                                            const double* s_inv, int64_t tbase) {
     double acc = 0.0;
@@ -85,16 +91,16 @@ __device__ __forceinline__ double rows_sum(const ScanSrc& s, int64_t bh, int64_t
     for (; r + SCAN_UNROLL <= r1; r += SCAN_UNROLL) {
         double v[SCAN_UNROLL];
 #pragma unroll
-        for (int u = 0; u < SCAN_UNROLL; ++u) v[u] = scan_value<MODE>(s, bh, N, r + u, c, s_inv[r + u - tbase]);
+        for (int u = 0; u < SCAN_UNROLL; ++u) v[u] = scan_value<MODE, TX>(s, bh, N, r + u, c, s_inv[r + u - tbase]);
 #pragma unroll
         for (int u = 0; u < SCAN_UNROLL; ++u) acc += v[u];
     }
-    for (; r < r1; ++r) acc += scan_value<MODE>(s, bh, N, r, c, s_inv[r - tbase]);
+    for (; r < r1; ++r) acc += scan_value<MODE, TX>(s, bh, N, r, c, s_inv[r - tbase]);
     return acc;
 }
 
 // (1) tile sums -> part[bh][tile][c]
-template <int MODE>
+template <int MODE, typename TX>
 __global__ void __launch_bounds__(SCAN_THREADS) scan_tile_sums_kernel(const ScanSrc s, int64_t N, int64_t ntile,
                                                                       int CW, double* __restrict__ part) {
     __shared__ double sh[SCAN_THREADS];
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_tile_sums_kernel(const Scan
         __syncthreads();
     }
     double acc = 0.0;
-    if (c < s.C) acc = rows_sum<MODE>(s, bh, N, r0, r1, c, s_inv, tile * SCAN_TB);
+    if (c < s.C) acc = rows_sum<MODE, TX>(s, bh, N, r0, r1, c, s_inv, tile * SCAN_TB);
     sh[threadIdx.x] = acc;
     __syncthreads();
     if (g == 0 && c < s.C) {
@@ -136,6 +142,7 @@ __global__ void scan_tiles_kernel(double* __restrict__ part, int64_t ntile, int 
 }
 
 // (3a) A4 apply: out[i] = (prefix through i) / (i + 1)  (causal only)
+template <typename TX>
 __global__ void __launch_bounds__(SCAN_THREADS) mean_apply_kernel(const ScanSrc s, int64_t N, int64_t ntile, int CW,
                                                                   const double* __restrict__ part,
                                                                   float* __restrict__ out) {
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) mean_apply_kernel(const ScanSrc 
     fill_inv(s_inv, tile);
     const bool on = c < s.C;
     double own = 0.0;
-    if (on) own = rows_sum<0>(s, bh, N, r0, r1, c, s_inv, tb);
+    if (on) own = rows_sum<0, TX>(s, bh, N, r0, r1, c, s_inv, tb);
     sh[threadIdx.x] = own;
     __syncthreads();
     if (!on) return;
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) mean_apply_kernel(const ScanSrc 
     for (; r + SCAN_UNROLL <= r1; r += SCAN_UNROLL) {
         double v[SCAN_UNROLL];
 #pragma unroll
-        for (int u = 0; u < SCAN_UNROLL; ++u) v[u] = scan_value<0>(s, bh, N, r + u, c, 1.0);
+        for (int u = 0; u < SCAN_UNROLL; ++u) v[u] = scan_value<0, TX>(s, bh, N, r + u, c, 1.0);
 #pragma unroll
         for (int u = 0; u < SCAN_UNROLL; ++u) {
             run += v[u];
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) mean_apply_kernel(const ScanSrc 
         }
     }
     for (; r < r1; ++r) {
-        run += scan_value<0>(s, bh, N, r, c, 1.0);
+        run += scan_value<0, TX>(s, bh, N, r, c, 1.0);
         out[(bh * N + r) * s.C + c] = (float)(run * s_inv[r - tb]);
     }
 }
@@ -179,12 +186,13 @@ __global__ void mean_global_kernel(const double* __restrict__ part, int64_t ntil
         out[bh * C + c] = (float)(part[(bh * (ntile + 1) + ntile) * C + c] / (double)N);
 }
 
-// (3b) A11 apply: D[t] += sum_{i >= t} y_i (causal, reverse walk) or
-// D[t] += (1/N) sum_i y_i (non-causal).
-template <int MODE>
+// (3b) A11 apply: out[t] = D[t] + sum_{i >= t} y_i (causal, reverse walk) or
+// out[t] = D[t] + (1/N) sum_i y_i (non-causal).  D is the key side's f32 result;
+// out is D itself (float rows) or the bf16 dV of a BF16 problem (one rounding).
+template <int MODE, typename TX, typename TO>
 __global__ void __launch_bounds__(SCAN_THREADS) grad_apply_kernel(const ScanSrc s, int64_t N, int64_t ntile, int CW,
                                                                   const double* __restrict__ part,
-                                                                  float* __restrict__ D) {
+                                                                  const float* D, TO* out) {
     __shared__ double sh[SCAN_THREADS];
     __shared__ double s_inv[SCAN_TB];
     const int64_t bh = blockIdx.y, tile = blockIdx.x;
@@ -197,15 +205,15 @@ __global__ void __launch_bounds__(SCAN_THREADS) grad_apply_kernel(const ScanSrc 
         if (!on) return;
         const double add = part[(bh * (ntile + 1) + ntile) * s.C + c] / (double)N;
         for (int64_t r = r0; r < r1; ++r) {
-            float* o = D + (bh * N + r) * s.C + c;
-            *o = (float)((double)*o + add);
+            const int64_t e = (bh * N + r) * s.C + c;
+            st1(out, e, (double)D[e] + add);
         }
         return;
     }
     fill_inv(s_inv, tile);
     __syncthreads();
     double own = 0.0;
-    if (on) own = rows_sum<MODE>(s, bh, N, r0, r1, c, s_inv, tb);
+    if (on) own = rows_sum<MODE, TX>(s, bh, N, r0, r1, c, s_inv, tb);
     sh[threadIdx.x] = own;
     __syncthreads();
     if (!on) return;
@@ -217,23 +225,23 @@ __global__ void __launch_bounds__(SCAN_THREADS) grad_apply_kernel(const ScanSrc 
         float d[SCAN_UNROLL];
 #pragma unroll
         for (int u = 0; u < SCAN_UNROLL; ++u) {
-            v[u] = scan_value<MODE>(s, bh, N, r - u, c, s_inv[r - u - tb]);
+            v[u] = scan_value<MODE, TX>(s, bh, N, r - u, c, s_inv[r - u - tb]);
             d[u] = D[(bh * N + r - u) * s.C + c];
         }
 #pragma unroll
         for (int u = 0; u < SCAN_UNROLL; ++u) {
             run += v[u];
-            D[(bh * N + r - u) * s.C + c] = (float)((double)d[u] + run);
+            st1(out, (bh * N + r - u) * s.C + c, (double)d[u] + run);
         }
     }
     for (; r >= r0; --r) {
-        run += scan_value<MODE>(s, bh, N, r, c, s_inv[r - tb]);
-        float* o = D + (bh * N + r) * s.C + c;
-        *o = (float)((double)*o + run);
+        run += scan_value<MODE, TX>(s, bh, N, r, c, s_inv[r - tb]);
+        const int64_t e = (bh * N + r) * s.C + c;
+        st1(out, e, (double)D[e] + run);
     }
 }
 
-cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const float* V, MeanBufs* m,
+cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const void* V, MeanBufs* m,
                                 cudaStream_t st) {
     const int64_t BH = p->B * p->H, N = p->N, nt = scan_tiles(p);
     const dim3 grid((unsigned)nt, (unsigned)BH);
@@ -242,13 +250,13 @@ cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const fl
     const ScanSrc sk{K, nullptr, nullptr, p->d_k, p->causal};
     const ScanSrc sv{V, nullptr, nullptr, p->d_v, p->causal};
     const int cwk = pow2_at_least(p->d_k), cwv = pow2_at_least(p->d_v);
-    scan_tile_sums_kernel<0><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
-    scan_tile_sums_kernel<0><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV);
+    scan_tile_sums_kernel<0, float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
+    ONEDF_DISPATCH_TV(p->vdtype, { scan_tile_sums_kernel<0, TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV); });
     scan_tiles_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, 0);
     scan_tiles_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, 0);
     if (p->causal) {
-        mean_apply_kernel<<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, m->Kbar);
-        mean_apply_kernel<<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, m->Vbar);
+        mean_apply_kernel<float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, m->Kbar);
+        ONEDF_DISPATCH_TV(p->vdtype, { mean_apply_kernel<TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, m->Vbar); });
     } else {
         mean_global_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, N, m->Kbar);
         mean_global_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, N, m->Vbar);
@@ -256,8 +264,8 @@ cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const fl
     return cudaGetLastError();
 }
 
-cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const float* dO, const float* muco,
-                                  MeanBufs* m, float* dK, float* dV, cudaStream_t st) {
+cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const void* dO, const float* muco,
+                                  MeanBufs* m, float* dK, const float* dV32, void* dV, cudaStream_t st) {
     const int64_t BH = p->B * p->H, N = p->N, nt = scan_tiles(p);
     const dim3 grid((unsigned)nt, (unsigned)BH);
     const float2* mc = reinterpret_cast<const float2*>(muco);
@@ -266,12 +274,28 @@ cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const 
     const ScanSrc sk{Q, m->Kbar, mc, p->d_k, p->causal, p->score == SC_DOT ? 0.0 : 1.0};
     const ScanSrc sv{dO, nullptr, mc, p->d_v, p->causal};
     const int cwk = pow2_at_least(p->d_k), cwv = pow2_at_least(p->d_v);
-    scan_tile_sums_kernel<1><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
-    scan_tile_sums_kernel<2><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV);
+    scan_tile_sums_kernel<1, float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
+    ONEDF_DISPATCH_TV(p->vdtype, { scan_tile_sums_kernel<2, TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV); });
     scan_tiles_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, 1);
     scan_tiles_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, 1);
-    grad_apply_kernel<1><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, dK);
-    grad_apply_kernel<2><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, dV);
+    grad_apply_kernel<1, float, float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, dK, dK);
+    ONEDF_DISPATCH_TV(p->vdtype, {
+        grad_apply_kernel<2, TV, TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, dV32, static_cast<TV*>(dV));
+    });
+    return cudaGetLastError();
+}
+
+// bf16 dV without the mean slot: one rounding of the key side's f32 rows
+__global__ void round_rows_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n4) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n4) return;
+    const float4 x = __ldg(reinterpret_cast<const float4*>(src) + t);
+    st4(dst, t, x.x, x.y, x.z, x.w);
+}
+
+cudaError_t launch_round_rows(const float* src, bf16* dst, int64_t n, cudaStream_t st) {
+    const int64_t n4 = n / 4;
+    if (n4 > 0) round_rows_kernel<<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(src, dst, n4);
     return cudaGetLastError();
 }
 

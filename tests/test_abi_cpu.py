@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(onedf):
     for name in _declared_functions():
         assert hasattr(lib, name), name
     assert set(onedf.abi.EXPORTS) == set(_declared_functions())
-    assert onedf.onedf_version() == 500
+    assert onedf.onedf_version() == 600
 
 
 def test_struct_layout_matches_c(onedf, tmp_path):
@@ -146,9 +146,9 @@ def test_calls_check_arguments_before_any_launch(onedf):
     good = onedf.Problem(*GOOD.values())
     assert lib.onedf_encode(ctypes.byref(bad), 1, 1, None, 1, 1, None, 256, 1 << 30, None) == onedf.abi.ERR_INVALID_ARG
     # workspace too small / misaligned / NULL -> ERR_WORKSPACE (checked before the device)
-    assert lib.onedf_topk_attn_fwd(ctypes.byref(good), *([256] * 10), 256, 16, None) == onedf.abi.ERR_WORKSPACE
+    assert lib.onedf_topk_attn_fwd(ctypes.byref(good), *([256] * 11), 256, 16, None) == onedf.abi.ERR_WORKSPACE
     assert lib.onedf_sort(ctypes.byref(good), 256, 256, 256, 257, 1 << 20, None) == onedf.abi.ERR_WORKSPACE
-    assert lib.onedf_topk_attn_bwd(ctypes.byref(good), *([256] * 14), None, 1 << 40, None) == onedf.abi.ERR_WORKSPACE
+    assert lib.onedf_topk_attn_bwd(ctypes.byref(good), *([256] * 15), None, 1 << 40, None) == onedf.abi.ERR_WORKSPACE
     assert onedf.status_string(onedf.abi.ERR_WORKSPACE).startswith("workspace")
 
 
@@ -167,3 +167,19 @@ def test_no_oracle_in_product_package():
             text = open(os.path.join(ROOT, "oracle", f)).read()
             for b in ("import paper_2501_14577_b200", "from paper_2501_14577_b200", "libonedf", "onedf.h"):
                 assert b not in text, (f, b)
+
+
+def test_bf16_contract_helpers():
+    """The bf16 parity helpers of tests/_util.py (NEXT-4, reading D26) against torch's own bfloat16:
+    rounding is round-to-nearest-even, and half_ulp(x) is half the gap to the next bf16 value."""
+    import numpy as np
+    import torch
+
+    from _util import bf16_half_ulp, bf16_round
+    x = np.array([1.0, 1.5, 3.0, 0.1, -7.25, 1e-3, 1.00390625, 1.01171875], dtype=np.float32)
+    r = bf16_round(x)
+    assert r[6] == 1.0 and r[7] == 1.015625            # ties to even: 1 + 2^-8 -> 1, 1 + 3*2^-8 -> 1 + 2^-6
+    b = torch.from_numpy(np.abs(r)).to(torch.bfloat16)
+    up = torch.nextafter(b, torch.full_like(b, float("inf"))).float().numpy()
+    np.testing.assert_array_equal(bf16_half_ulp(r), (up - np.abs(r)) / 2)
+    assert bf16_half_ulp(0.0) == 0.0

@@ -324,7 +324,8 @@ def test_autograd_function_and_host_step():
 
 @pytest.mark.parametrize("name", ["ar_tokens", "lra_nc"])
 def test_schedule_hints_do_not_change_results(name):
-    """qcode/perm only pick the visiting order of the backward: outputs are bitwise identical."""
+    """qcode/qorder/perm only pick the visiting order of the forward and backward (any per-chunk
+    permutation, e.g. the natural order): outputs are bitwise identical."""
     import torch
 
     import paper_2501_14577_b200 as onedf
@@ -340,12 +341,22 @@ def test_schedule_hints_do_not_change_results(name):
     qc, kc, _ = onedf.encode(p, t["Q"], t["K"], ws=ws)
     sc, pm = onedf.sort(p, kc, ws=ws)
     O, idx, Z = onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws)
+    # the forward with the caller's schedule (onedf_sort of qcode) or the natural order: same bits
+    qo = onedf.query_schedule(p, qc, ws=ws)
+    fwd_a = [v.cpu().numpy().copy() for v in (O, idx, Z)]
+    nat = torch.arange(p.N, dtype=torch.int32, device=dev).expand(p.B, p.H, p.N).contiguous()
+    for hint in (qo, nat):
+        fwd_b = [v.cpu().numpy() for v in onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws,
+                                                              qorder=hint)]
+        for u, v, n in zip(fwd_a, fwd_b, ("O", "idx", "Z")):
+            assert np.array_equal(u.view(np.uint8), v.view(np.uint8)), n
     a = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws, qcode=qc, perm=pm)
     a = [v.cpu().numpy().copy() for v in a]
-    b = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws)
-    b = [v.cpu().numpy() for v in b]
-    for u, v, n in zip(a, b, ("dQ", "dK", "dV", "d_eps")):
-        assert np.array_equal(np.atleast_1d(u).view(np.uint8), np.atleast_1d(v).view(np.uint8)), n
+    for hints in ({}, {"qorder": qo, "perm": pm}, {"qorder": nat}):
+        b = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws, **hints)
+        b = [v.cpu().numpy() for v in b]
+        for u, v, n in zip(a, b, ("dQ", "dK", "dV", "d_eps")):
+            assert np.array_equal(np.atleast_1d(u).view(np.uint8), np.atleast_1d(v).view(np.uint8)), (n, hints)
 
 
 def test_host_step_pipelined_groups_match_device_path():
