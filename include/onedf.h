@@ -180,7 +180,8 @@ onedf_status onedf_project_encode(const onedf_problem* p, int32_t d_model, const
  *   dWq[h] = sum_{b,n} dq x^T, dWk likewise   [H, d_k, d_model]
  *   dbq[h] = sum_{b,n} dq, dbk likewise       [H, d_k] (nullable)
  *   dtheta = d_eps sigma(theta) (1 - sigma(theta))   device float (nullable)
- * dW/db sum fixed row groups in a fixed order (bitwise reproducible).
+ * dW/db sum fixed row groups in a fixed order (bitwise reproducible).  dX needs
+ * 2 H d_k <= 128 (its kernel stages every output column on chip), else UNSUPPORTED.
  * Workspace: onedf_project_workspace_size(p, d_model). */
 size_t onedf_project_workspace_size(const onedf_problem* p, int32_t d_model);
 onedf_status onedf_project_bwd(const onedf_problem* p, int32_t d_model, const float* X,

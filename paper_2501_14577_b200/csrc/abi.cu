@@ -430,6 +430,7 @@ onedf_status onedf_project_bwd(const onedf_problem* p, int32_t d_model, const fl
         return ONEDF_ERR_WORKSPACE;
     if ((s = check_device()) != ONEDF_OK) return s;
     if (!X || !Wq || !Wk || !dQ || !dK || !dWq || !dWk || (dtheta && (!theta || !d_eps))) return ONEDF_ERR_INVALID_ARG;
+    if (dX && 2 * p->H * p->d_k > 128) return ONEDF_ERR_UNSUPPORTED;    // dX stages all 2 H d_k columns on chip
     return finish(launch_project_bwd(p, d_model, X, Wq, Wk, theta, dQ, dK, d_eps, dX, dWq, dWk, dbq, dbk, dtheta, ws,
                                      (cudaStream_t)stream));
 }

@@ -108,10 +108,8 @@ __global__ void __launch_bounds__(PJ_THREADS, 2) project_kernel(const ProjArgs a
     }
 }
 
-// dX = sum_o dY[., o] W[o, .] with dY[(b,n), o] = dq_{b,h,n,d} / dk_{b,h,n,d}.  CTA: PJ_ROWS rows x
-// 64 d_model columns; thread (ty, tx) owns rows ty + 32 i and columns tx + 8 c (c < 8); the O
-// axis is walked in slices of PJB_OC with dY and W staged in shared memory as f64.
-constexpr int PJB_OC = 24;
+// dX = sum_o dY[., o] W[o, .] with dY[(b,n), o] = dq_{b,h,n,d} / dk_{b,h,n,d}.  CTA: PJ_ROWS rows;
+// thread (ty, tx) owns rows ty + 32 i and, per d_model tile of PJB_MT, columns tx + 8 c (c < 8).
 constexpr int PJB_MT = 64;
 
 struct ProjBwdArgs {
@@ -122,13 +120,17 @@ struct ProjBwdArgs {
     int64_t B, H, N; int dk, dm, G;
 };
 
-__device__ __forceinline__ float dy_value(const ProjBwdArgs& a, int64_t r, int o) {
+// dY column o (a q or k coordinate (h, d)) as a base pointer: dY[r][o] = col[o][rowoff(r)], with
+// rowoff(b, n) = (b H N + n) d_k -- the 64-bit index split once per column and once per row, so the
+// staging loops do no division.
+__device__ __forceinline__ const float* dy_col(const ProjBwdArgs& a, int o) {
     const int hd = (int)a.H * a.dk;
     const bool isq = o < hd;
     const int oo = isq ? o : o - hd;
-    const int h = oo / a.dk, d = oo % a.dk;
-    const int64_t b = r / a.N, n = r % a.N;
-    return __ldg((isq ? a.dQ : a.dK) + ((b * a.H + h) * a.N + n) * a.dk + d);
+    return (isq ? a.dQ : a.dK) + ((int64_t)(oo / a.dk) * a.N) * a.dk + oo % a.dk;
+}
+__device__ __forceinline__ int64_t dy_rowoff(const ProjBwdArgs& a, int64_t r) {
+    return ((r / a.N) * a.H * a.N + r % a.N) * a.dk;
 }
 
 __device__ __forceinline__ const float* w_row_b(const ProjBwdArgs& a, int o) {
@@ -136,93 +138,116 @@ __device__ __forceinline__ const float* w_row_b(const ProjBwdArgs& a, int o) {
     return (o < hd ? a.Wq : a.Wk) + (int64_t)(o < hd ? o : o - hd) * a.dm;
 }
 
+// dX: the CTA stages its rows' whole dY tile [PJ_ROWS x O] once (f64, dynamic shared memory) and
+// walks d_model in tiles of PJB_MT columns, staging W[:, tile] for each.
 __global__ void __launch_bounds__(PJ_THREADS, 2) project_dx_kernel(const ProjBwdArgs a) {
-    __shared__ double ys[PJ_ROWS][PJB_OC + 1];
-    __shared__ double wsm[PJB_OC][PJB_MT + 1];
+    extern __shared__ double dsm[];
+    const int O = 2 * (int)a.H * a.dk;
+    const int OS = O + 1;                                   // row stride of ys (odd: no bank conflicts)
+    double* ys = dsm;                                       // [PJ_ROWS][OS]
+    double* wsm = dsm + PJ_ROWS * OS;                       // [O][PJB_MT + 1]
+    __shared__ int64_t s_row[PJ_ROWS];
     const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
     const int64_t rows = a.B * a.N;
     const int64_t r0 = (int64_t)blockIdx.x * PJ_ROWS;
-    const int m0 = blockIdx.y * PJB_MT;
-    const int O = 2 * (int)a.H * a.dk;
-    double acc[PJ_RT][8];
-#pragma unroll
-    for (int i = 0; i < PJ_RT; ++i)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) acc[i][c] = 0.0;
-    for (int oc = 0; oc < O; oc += PJB_OC) {
+    for (int r = threadIdx.x; r < PJ_ROWS; r += PJ_THREADS) s_row[r] = r0 + r < rows ? dy_rowoff(a, r0 + r) : -1;
+    __syncthreads();
+    for (int o = threadIdx.x / 32; o < O; o += PJ_THREADS / 32) {           // a warp per column
+        const float* col = dy_col(a, o);
+        for (int r = threadIdx.x % 32; r < PJ_ROWS; r += 32)
+            ys[r * OS + o] = s_row[r] >= 0 ? (double)__ldg(col + s_row[r]) : 0.0;
+    }
+    for (int m0 = 0; m0 < a.dm; m0 += PJB_MT) {
         __syncthreads();
-        for (int t = threadIdx.x; t < PJ_ROWS * PJB_OC; t += PJ_THREADS) {
-            const int r = t / PJB_OC, o = t % PJB_OC;
-            ys[r][o] = (r0 + r < rows && oc + o < O) ? (double)dy_value(a, r0 + r, oc + o) : 0.0;
-        }
-        for (int t = threadIdx.x; t < PJB_OC * PJB_MT; t += PJ_THREADS) {
+        for (int t = threadIdx.x; t < O * PJB_MT; t += PJ_THREADS) {
             const int o = t / PJB_MT, m = t % PJB_MT;
-            wsm[o][m] = (oc + o < O && m0 + m < a.dm) ? (double)__ldg(w_row_b(a, oc + o) + m0 + m) : 0.0;
+            wsm[o * (PJB_MT + 1) + m] = m0 + m < a.dm ? (double)__ldg(w_row_b(a, o) + m0 + m) : 0.0;
         }
         __syncthreads();
+        double acc[PJ_RT][8];
+#pragma unroll
+        for (int i = 0; i < PJ_RT; ++i)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[i][c] = 0.0;
 #pragma unroll 4
-        for (int o = 0; o < PJB_OC; ++o) {
+        for (int o = 0; o < O; ++o) {
             double y[PJ_RT], w[8];
 #pragma unroll
-            for (int i = 0; i < PJ_RT; ++i) y[i] = ys[ty + 32 * i][o];
+            for (int i = 0; i < PJ_RT; ++i) y[i] = ys[(ty + 32 * i) * OS + o];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) w[c] = wsm[o][tx + 8 * c];
+            for (int c = 0; c < 8; ++c) w[c] = wsm[o * (PJB_MT + 1) + tx + 8 * c];
 #pragma unroll
             for (int i = 0; i < PJ_RT; ++i)
 #pragma unroll
                 for (int c = 0; c < 8; ++c) acc[i][c] = fma(y[i], w[c], acc[i][c]);
         }
-    }
 #pragma unroll
-    for (int i = 0; i < PJ_RT; ++i) {
-        const int64_t r = r0 + ty + 32 * i;
-        if (r >= rows) continue;
+        for (int i = 0; i < PJ_RT; ++i) {
+            const int64_t r = r0 + ty + 32 * i;
+            if (r >= rows) continue;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            const int m = m0 + tx + 8 * c;
-            if (m < a.dm) a.dX[r * a.dm + m] = (float)acc[i][c];
+            for (int c = 0; c < 8; ++c) {
+                const int m = m0 + tx + 8 * c;
+                if (m < a.dm) a.dX[r * a.dm + m] = (float)acc[i][c];
+            }
         }
     }
 }
 
-// dW / db partials: row group g (a fixed contiguous range of the B*N rows, G groups whatever the
-// device) x PJ_COLS output columns x 64 d_model columns; thread (to, tm) owns outputs to + 8 c and
-// columns tm + 32 u (u < 2); rows are walked in slices of 32 in ascending order (fixed order).
-// Column d_model of the partial holds db (the tm == 0 threads of the m-tile 0 CTAs).
-__global__ void __launch_bounds__(PJ_THREADS) project_dw_partial_kernel(const ProjBwdArgs a) {
+static size_t dx_smem(int O) { return sizeof(double) * ((size_t)PJ_ROWS * (O + 1) + (size_t)O * (PJB_MT + 1)); }
+
+// dW partials: row group g (a fixed contiguous range of the B*N rows, G groups whatever the device)
+// x PJ_COLS output columns x PJW_MT d_model columns; thread (to, tm) owns outputs to + 8 c (c < 9)
+// and columns tm + 32 u (u < 4); rows are walked in slices of 32 in ascending order (fixed order).
+// The m-tile 0 CTAs also sum db (column d_model of the partial rows).
+constexpr int PJW_MT = 128;
+__global__ void __launch_bounds__(PJ_THREADS, 2) project_dw_partial_kernel(const ProjBwdArgs a) {
     __shared__ double ys[32][PJ_COLS + 1];
-    __shared__ float xs[32][PJB_MT + 1];
+    __shared__ float xs[32][PJW_MT + 4];
+    __shared__ int64_t s_row[32];
+    __shared__ const float* s_col[PJ_COLS];
     const int tm = threadIdx.x % 32, to = threadIdx.x / 32;    // 32 x 8
     const int64_t rows = a.B * a.N;
     const int g = blockIdx.x;
     const int64_t per = (rows + a.G - 1) / a.G;
     const int64_t ra = (int64_t)g * per, rb = min64(rows, ra + per);
-    const int m0 = blockIdx.y * PJB_MT, o0 = blockIdx.z * PJ_COLS;
+    const int m0 = blockIdx.y * PJW_MT, o0 = blockIdx.z * PJ_COLS;
     const int O = 2 * (int)a.H * a.dk;
-    const bool with_db = blockIdx.y == 0;
-    double acc[PJ_CT][2], accb[PJ_CT];
+    for (int o = threadIdx.x; o < PJ_COLS; o += PJ_THREADS) s_col[o] = o0 + o < O ? dy_col(a, o0 + o) : nullptr;
+    const bool with_db = blockIdx.y == 0 && threadIdx.x < PJ_COLS;
+    double dbacc = 0.0;                             // thread t < PJ_COLS: db of column o0 + t
+    double acc[PJ_CT][4];
 #pragma unroll
-    for (int c = 0; c < PJ_CT; ++c) { acc[c][0] = acc[c][1] = 0.0; accb[c] = 0.0; }
+    for (int c = 0; c < PJ_CT; ++c)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[c][u] = 0.0;
     for (int64_t s = ra; s < rb; s += 32) {
         __syncthreads();
-        for (int t = threadIdx.x; t < 32 * PJ_COLS; t += PJ_THREADS) {
-            const int r = t / PJ_COLS, o = t % PJ_COLS;
-            ys[r][o] = (s + r < rb && o0 + o < O) ? (double)dy_value(a, s + r, o0 + o) : 0.0;
-        }
-        for (int t = threadIdx.x; t < 32 * PJB_MT; t += PJ_THREADS) {
-            const int r = t / PJB_MT, m = t % PJB_MT;
+        if (threadIdx.x < 32) s_row[threadIdx.x] = s + threadIdx.x < rb ? dy_rowoff(a, s + threadIdx.x) : -1;
+        for (int t = threadIdx.x; t < 32 * PJW_MT; t += PJ_THREADS) {
+            const int r = t / PJW_MT, m = t % PJW_MT;
             xs[r][m] = (s + r < rb && m0 + m < a.dm) ? __ldg(a.X + (s + r) * a.dm + m0 + m) : 0.f;
         }
         __syncthreads();
+        for (int t = threadIdx.x; t < 32 * PJ_COLS; t += PJ_THREADS) {
+            const int r = t / PJ_COLS, o = t % PJ_COLS;
+            const float* col = s_col[o];
+            ys[r][o] = (s_row[r] >= 0 && col) ? (double)__ldg(col + s_row[r]) : 0.0;
+        }
+        __syncthreads();
+        if (with_db)
+            for (int r = 0; r < 32; ++r) dbacc += ys[r][threadIdx.x];
+#pragma unroll 2
         for (int r = 0; r < 32; ++r) {
-            const double x0 = (double)xs[r][tm], x1 = (double)xs[r][tm + 32];
+            double x[4], y[PJ_CT];
 #pragma unroll
-            for (int c = 0; c < PJ_CT; ++c) {
-                const double y = ys[r][to + 8 * c];
-                acc[c][0] = fma(y, x0, acc[c][0]);
-                acc[c][1] = fma(y, x1, acc[c][1]);
-                accb[c] += y;
-            }
+            for (int u = 0; u < 4; ++u) x[u] = (double)xs[r][tm + 32 * u];
+#pragma unroll
+            for (int c = 0; c < PJ_CT; ++c) y[c] = ys[r][to + 8 * c];
+#pragma unroll
+            for (int c = 0; c < PJ_CT; ++c)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc[c][u] = fma(y[c], x[u], acc[c][u]);
         }
     }
     const int64_t stride = (int64_t)a.dm + 1;
@@ -231,10 +256,11 @@ __global__ void __launch_bounds__(PJ_THREADS) project_dw_partial_kernel(const Pr
         const int o = o0 + to + 8 * c;
         if (o >= O) continue;
         double* prow = a.part + ((int64_t)g * O + o) * stride;
-        if (m0 + tm < a.dm) prow[m0 + tm] = acc[c][0];
-        if (m0 + tm + 32 < a.dm) prow[m0 + tm + 32] = acc[c][1];
-        if (with_db && tm == 0) prow[a.dm] = accb[c];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (m0 + tm + 32 * u < a.dm) prow[m0 + tm + 32 * u] = acc[c][u];
     }
+    if (with_db && o0 + (int)threadIdx.x < O) a.part[((int64_t)g * O + o0 + threadIdx.x) * stride + a.dm] = dbacc;
 }
 
 // dW, db = the G row-group partials summed in group order; dtheta = d_eps sigma (1 - sigma).
@@ -258,7 +284,7 @@ __global__ void project_dw_reduce_kernel(const ProjBwdArgs a) {
     }
 }
 
-constexpr int PJ_GROUPS = 64;          // row groups of the dW reduction (fixed: deterministic everywhere)
+constexpr int PJ_GROUPS = 148;         // row groups of the dW reduction (fixed: deterministic on any device)
 
 size_t project_ws_bytes(const onedf_problem* p, int d_model, Carver* c) {
     const int64_t O = 2 * p->H * (int64_t)p->d_k;
@@ -292,10 +318,14 @@ cudaError_t launch_project_bwd(const onedf_problem* p, int d_model, const float*
     const int O = 2 * (int)p->H * p->d_k;
     const int64_t rows = p->B * p->N;
     if (dX) {
-        const dim3 gx((unsigned)((rows + PJ_ROWS - 1) / PJ_ROWS), (unsigned)((d_model + PJB_MT - 1) / PJB_MT));
-        project_dx_kernel<<<gx, PJ_THREADS, 0, st>>>(a);
+        const size_t smem = dx_smem(O);
+        if (smem > 200 * 1024) return cudaErrorNotSupported;                  // O <= ~130 (validated)
+        cudaError_t e = cudaFuncSetAttribute(project_dx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        project_dx_kernel<<<(unsigned)((rows + PJ_ROWS - 1) / PJ_ROWS), PJ_THREADS, smem, st>>>(a);
     }
-    const dim3 gw((unsigned)PJ_GROUPS, (unsigned)((d_model + PJB_MT - 1) / PJB_MT), (unsigned)((O + PJ_COLS - 1) / PJ_COLS));
+    const dim3 gw((unsigned)PJ_GROUPS, (unsigned)((d_model + PJW_MT - 1) / PJW_MT), (unsigned)((O + PJ_COLS - 1) / PJ_COLS));
     project_dw_partial_kernel<<<gw, PJ_THREADS, 0, st>>>(a);
     project_dw_reduce_kernel<<<148, 256, 0, st>>>(a);
     return cudaGetLastError();
