@@ -42,10 +42,15 @@ cudaError_t launch_bounds_finish(const onedf_problem* p, double* lohi, void* ws,
 cudaError_t launch_rank_sum(const float* parts, int64_t n, int32_t world, float* out, cudaStream_t st);
 
 // sort.cu
-// Global ping-pong scratch of the run sort, only for runs longer than SEG_SORT_MAX (else null).
+// Global scratch of the onesweep sort of runs longer than SEG_SORT_MAX (else null): ping-pong
+// keys/positions, per-(run, pass) digit bases, per-(run, tile, digit) look-back status words and the
+// per-pass tile tickets.
 struct SortScratch {
     uint64_t* k[2];
     uint32_t* v[2];
+    uint32_t* base;     // [runs][8][256]  digit counts -> exclusive digit offsets per pass
+    uint32_t* status;   // [runs][tiles][256] decoupled look-back words (flag << 30 | count)
+    uint32_t* ticket;   // [8]             dynamic tile order per pass
 };
 void sort_carve(const onedf_problem* p, Carver* c, SortScratch* s);
 cudaError_t launch_seg_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t* scode /* nullable */,

@@ -382,3 +382,36 @@ def test_host_step_pipelined_groups_match_device_path():
         for n in ("O", "dQ", "dK", "dV"):
             assert np.array_equal(outs[n].numpy(), ref[n]), n
         assert float(d_eps) == pytest.approx(float(ref["d_eps"]), rel=1e-12)
+
+
+@pytest.mark.parametrize("N,d_k,tokens", [(1 << 20, 3, False), (200_003, 2, False), (50_000, 3, True),
+                                          (8193, 1, False)])
+def test_onesweep_long_run_sort(N, d_k, tokens):
+    """Runs longer than onedf_max_run_length() go through the multi-CTA onesweep radix sort
+    (decoupled look-back): a single non-causal run of up to 1M keys, ragged tile counts, heavy
+    code ties (repeated tokens) and a one-key-past-the-limit run -- scode and perm bit-exact
+    against the oracle's std::sort on (code, position), for the key codes and the query schedule."""
+    import torch
+
+    import paper_2501_14577_b200 as onedf
+    kw = dict(B=1, H=1, N=N, d_k=d_k, d_v=4, k=4, window=8, chunk=1, causal=0, mean_slot=0)
+    rng = np.random.default_rng(N)
+    Q = rng.normal(size=(1, 1, N, d_k)).astype(np.float32)
+    K = rng.normal(size=(1, 1, N, d_k)).astype(np.float32)
+    if tokens:
+        vocab = rng.normal(size=(97, d_k)).astype(np.float32)
+        K = vocab[rng.integers(0, 97, size=(1, 1, N))]
+    p = oracle.Problem(**kw)
+    qc, kc, _ = oracle.encode(p, Q, K)
+    sc_ref, pm_ref = oracle.sort(p, kc)
+    _, qo_ref = oracle.sort(p, qc)
+    dev = torch.device("cuda:0")
+    pg = onedf.make_problem(**kw)
+    ws = onedf.Workspace(dev)
+    kc_t = torch.from_numpy(kc.view(np.int64)).to(dev)
+    sc, pm = onedf.sort(pg, kc_t, ws=ws)
+    qo = onedf.query_schedule(pg, torch.from_numpy(qc.view(np.int64)).to(dev), ws=ws)
+    torch.cuda.synchronize()
+    assert_same(sc.cpu().numpy().view(np.uint64), sc_ref, "scode")
+    assert_same(pm.cpu().numpy(), pm_ref, "perm")
+    assert_same(qo.cpu().numpy(), qo_ref, "qorder")
