@@ -54,8 +54,10 @@ def _headers():
     return hs
 
 
-def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, objdir: str = OBJDIR) -> str:
-    """defines/lib/objdir: variant builds for tools/ experiments (the product is the default)."""
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, objdir: str = OBJDIR,
+          define_srcs=None) -> str:
+    """defines/lib/objdir: variant builds for tools/ experiments (the product is the default);
+    define_srcs: apply the defines only to the units of these sources (others as in the product)."""
     os.makedirs(objdir, exist_ok=True)
     hdrs = _headers()
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
@@ -68,9 +70,10 @@ def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB
         o = os.path.join(objdir, obj + ".o")
         # per-object content stamp (source + every header + flags + defines): an object is reused
         # only if it was built from exactly these inputs, whatever the files' mtimes say
-        ostamp = _stamp([s] + hdrs, tuple(defines) + tuple(udefs))
+        defs = tuple(defines) if define_srcs is None or src in define_srcs else ()
+        ostamp = _stamp([s] + hdrs, defs + tuple(udefs))
         if force or not os.path.exists(o) or _read(o + ".stamp") != ostamp:
-            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in tuple(defines) + tuple(udefs)], "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defs + tuple(udefs)], "-c", s, "-o", o]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((cmd, o, ostamp))

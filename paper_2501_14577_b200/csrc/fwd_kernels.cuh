@@ -27,6 +27,10 @@ constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 l
 #define ONEDF_FWD_TBITS 18                          // bisection of T stops at 2^(TBITS-23) relative width
 #endif
 constexpr int FWD_CAP = 256;                        // pass-2 collection capacity per warp
+#ifndef ONEDF_FWD_SUB
+#define ONEDF_FWD_SUB 4
+#endif
+constexpr int FWD_SUB = ONEDF_FWD_SUB;              // pass 1 samples every FWD_SUB-th run (1: all runs)
 constexpr unsigned long long KEY_MAX = ~0ull;
 
 // ------------------------------------------------------------------ register top-k
@@ -161,8 +165,9 @@ struct CandSet {
 
     // f(D[FWD_UB], j[FWD_UB], valid[FWD_UB]) per stretch; returns false to stop.
     // (base0, w0) are the lane-parallel windows of runs 0..31, computed once.
+    // stride > 1: only the runs c with c % stride == 0 (pass 1's sampled bound).
     template <class F>
-    __device__ __forceinline__ bool visit(int64_t base0, int w0, F&& f) const {
+    __device__ __forceinline__ bool visit(int64_t base0, int w0, F&& f, int stride = 1) const {
         constexpr int REC = RecW<DK>::value;
         const int lane = lane_id();
         for (int64_t c0 = 0; c0 < nruns; c0 += 32) {
@@ -171,6 +176,7 @@ struct CandSet {
             if (c0 > 0) window(c0 + lane, base, w);
             const int nc = (int)min64(32, nruns - c0);
             for (int cc = 0; cc < nc; ++cc) {
+                if (stride > 1 && (c0 + cc) % stride != 0) continue;     // warp-uniform
                 const int b = (int)__shfl_sync(FULL, base, cc);
                 const int ww = __shfl_sync(FULL, w, cc);
                 const float4* wp = recs4 + (b + lane) * (REC / 4);
@@ -346,73 +352,100 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         int w0;
         cs.window(lane, base0, w0);
 
-        // ---------------- A6 pass 1: per-lane L smallest D (f32 min/max chain).
-        // The k-th smallest of the union of these lists is an upper bound T on
-        // the k-th smallest D of C_i (k distinct candidates lie at or below it).
-        float lst[L];
+        // ---------------- A6 pass 1 (pass_one): per-lane L smallest D (f32 min/max chain) over the
+        // runs c % stride == 0, then T = (about) the target-th smallest of their union.
+        auto pass_one = [&](int stride, int target) -> unsigned {
+            // The k-th smallest of the union of these lists is an upper bound T on
+            // the k-th smallest D of C_i (k distinct candidates lie at or below it).
+            float lst[L];
 #pragma unroll
-        for (int t = 0; t < L; ++t) lst[t] = INFINITY;
-        cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&)[FWD_UB], const bool (&ok)[FWD_UB], int, int) {
+            for (int t = 0; t < L; ++t) lst[t] = INFINITY;
+            cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&)[FWD_UB], const bool (&ok)[FWD_UB], int, int) {
 #pragma unroll
-            for (int uu = 0; uu < FWD_UB; ++uu) {
-                float x = ok[uu] ? D[uu] : INFINITY;
+                for (int uu = 0; uu < FWD_UB; ++uu) {
+                    float x = ok[uu] ? D[uu] : INFINITY;
 #pragma unroll
-                for (int t = 0; t < L; ++t) {
-                    const float lo = fminf(lst[t], x);
-                    x = fmaxf(lst[t], x);
-                    lst[t] = lo;
+                    for (int t = 0; t < L; ++t) {
+                        const float lo = fminf(lst[t], x);
+                        x = fmaxf(lst[t], x);
+                        lst[t] = lo;
+                    }
                 }
-            }
-            return true;
-        });
-        // T: a bit pattern with #{values <= T} >= k (non-negative floats order as
-        // their bits).  Bisection between the smallest list head and the largest
-        // list tail, stopped at 2^(TBITS-23) relative width: any such T is a valid
-        // bound, a slightly larger one only admits a few more keys in pass 2.
-        unsigned tb;
-        {
-            float fmn = lst[0], fmx = lst[L - 1];
-            unsigned finite = 0;
+                return true;
+            }, stride);
+            // T: a bit pattern with #{values <= T} >= k (non-negative floats order as
+            // their bits).  Bisection between the smallest list head and the largest
+            // list tail, stopped at 2^(TBITS-23) relative width: any such T is a valid
+            // bound, a slightly larger one only admits a few more keys in pass 2.
+            unsigned tb;
+            {
+                float fmn = lst[0], fmx = lst[L - 1];
+                unsigned finite = 0;
 #pragma unroll
-            for (int t = 0; t < L; ++t) finite += lst[t] < INFINITY;
+                for (int t = 0; t < L; ++t) finite += lst[t] < INFINITY;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) fmn = fminf(fmn, __shfl_xor_sync(FULL, fmn, o));
+                for (int o = 16; o > 0; o >>= 1) fmn = fminf(fmn, __shfl_xor_sync(FULL, fmn, o));
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
-            if (__reduce_add_sync(FULL, finite) < (unsigned)k) {
-                tb = 0x7f800000u;                          // fewer than k candidates: admit all
-            } else {
-                unsigned lo = __float_as_uint(fmn), hi = __float_as_uint(fmx);   // count(<= hi) >= k
+                for (int o = 16; o > 0; o >>= 1) fmx = fmaxf(fmx, __shfl_xor_sync(FULL, fmx, o));
+                if (__reduce_add_sync(FULL, finite) < (unsigned)target) {
+                    tb = 0x7f800000u;                          // fewer than k candidates: admit all
+                } else {
+                    unsigned lo = __float_as_uint(fmn), hi = __float_as_uint(fmx);   // count(<= hi) >= target
 #pragma unroll 1
-                while (hi - lo > (1u << ONEDF_FWD_TBITS)) {   // stop at 2^(TBITS-23) relative resolution
-                    const unsigned mid = lo + ((hi - lo) >> 1);
-                    unsigned c = 0;
+                    while (hi - lo > (1u << ONEDF_FWD_TBITS)) {   // stop at 2^(TBITS-23) relative resolution
+                        const unsigned mid = lo + ((hi - lo) >> 1);
+                        unsigned c = 0;
 #pragma unroll
-                    for (int t = 0; t < L; ++t) c += __float_as_uint(lst[t]) <= mid;
-                    if (__reduce_add_sync(FULL, c) >= (unsigned)k) hi = mid; else lo = mid + 1;
+                        for (int t = 0; t < L; ++t) c += __float_as_uint(lst[t]) <= mid;
+                        if (__reduce_add_sync(FULL, c) >= (unsigned)target) hi = mid; else lo = mid + 1;
+                    }
+                    tb = hi;
                 }
-                tb = hi;
             }
+            return tb;
+        };
+        // The bound only has to admit >= k candidates, which pass 2 counts exactly, so it may be a
+        // guess: the (mult * k * sampled/all)-th smallest D of every FWD_SUB-th run (mult = 3/2)
+        // admits ~1.5 k keys and is too small for ~2 % of the long64k queries (CPU simulation, DESIGN
+        // section 7); those redo pass 1 over every run.  A guess admitting more than FWD_CAP keys
+        // (repeated tokens: many equal distances) goes to the streaming selection below, whose
+        // threshold tightens to the k-th key as soon as k keys are in.  Exactness never depends on
+        // the guess.
+        const bool sampled = FWD_SUB > 1 && cs.nruns >= 2 * FWD_SUB;
+        unsigned tb;
+        if (sampled) {
+            const int nsub = (int)((cs.nruns + FWD_SUB - 1) / FWD_SUB);
+            const int target = (int)((3 * (int64_t)k * nsub + 2 * cs.nruns - 1) / (2 * cs.nruns));
+            tb = pass_one(FWD_SUB, target < 1 ? 1 : target);
+        } else {
+            tb = pass_one(1, k);
         }
 
         // ---------------- A6 pass 2: collect every candidate with D <= T (order is
         // irrelevant: the final order comes from ranking the unique keys)
-        int cnt = 0;
-        if (lane == 0) s_cnt[warp] = 0;
-        __syncwarp();
-        cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB], const bool (&ok)[FWD_UB], int,
-                                int) {
+        auto collect = [&]() -> int {
+            if (lane == 0) s_cnt[warp] = 0;
+            __syncwarp();
+            cs.visit(base0, w0, [&](const float (&D)[FWD_UB], const int (&jj)[FWD_UB], const bool (&ok)[FWD_UB], int,
+                                    int) {
 #pragma unroll
-            for (int uu = 0; uu < FWD_UB; ++uu) {
-                if (ok[uu] && __float_as_uint(D[uu]) <= tb) {
-                    const int pos = atomicAdd(&s_cnt[warp], 1);
-                    if (pos < FWD_CAP) buf[pos] = make_key(D[uu], jj[uu]);
+                for (int uu = 0; uu < FWD_UB; ++uu) {
+                    if (ok[uu] && __float_as_uint(D[uu]) <= tb) {
+                        const int pos = atomicAdd(&s_cnt[warp], 1);
+                        if (pos < FWD_CAP) buf[pos] = make_key(D[uu], jj[uu]);
+                    }
                 }
-            }
-            return true;
-        });
-        __syncwarp();
-        cnt = s_cnt[warp];
+                return true;
+            });
+            __syncwarp();
+            return s_cnt[warp];
+        };
+        int cnt = collect();
+        if (sampled && cnt < k) {
+            __syncwarp();
+            tb = pass_one(1, k);
+            cnt = collect();
+        }
         const bool fits = cnt <= FWD_CAP;
 #ifdef ONEDF_FWD_STATS
         if (lane == 0) {

@@ -1,11 +1,12 @@
 """Build variant libraries (same sources, different tuning macros) under build_variants/.
 
     python tools/variants.py [--src fwd.cu,bwd.cu] NAME=DEF1,DEF2 ...
-        e.g.  python tools/variants.py --src fwd.cu ub2_b3=ONEDF_FWD_UB=2,ONEDF_FWD_MINB=3
-              (backward kernel macros: --src bwd_dk12.cu,bwd_dk34.cu,bwd_dk56.cu,bwd_dk78.cu)
+        e.g.  python tools/variants.py --src fwd_inst.cu sub2=ONEDF_FWD_SUB=2
+              (backward kernel macros: --src bwd_inst.cu)
 Each lands in build_variants/NAME/libonedf.so; select one with ONEDF_LIB=... (tools only).
-With --src only those sources are recompiled with the defines; the other objects are
-copied from the product build (paper_2501_14577_b200/build/), which must be current.
+With --src only the compilation units of those sources are recompiled with the defines; the
+other objects are copied from the product build (paper_2501_14577_b200/build/), which must be
+current.
 """
 import argparse
 import importlib.util
@@ -27,11 +28,13 @@ for arg in a.variants:
     d = os.path.join(ROOT, "build_variants", name)
     os.makedirs(d, exist_ok=True)
     if only:
-        for src in b.SOURCES:
-            o = src.replace(".cu", ".o")
+        for obj, src, _ in b.UNITS:
+            o = obj + ".o"
             if src in only:
                 if os.path.exists(os.path.join(d, o)):
                     os.remove(os.path.join(d, o))
             else:
                 shutil.copy2(os.path.join(b.OBJDIR, o), os.path.join(d, o))
-    print(b.build(defines=[x for x in defs.split(",") if x], lib=os.path.join(d, "libonedf.so"), objdir=d))
+                shutil.copy2(os.path.join(b.OBJDIR, o + ".stamp"), os.path.join(d, o + ".stamp"))
+    print(b.build(defines=[x for x in defs.split(",") if x], lib=os.path.join(d, "libonedf.so"), objdir=d,
+                  define_srcs=only or None))
