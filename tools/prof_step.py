@@ -35,12 +35,13 @@ def main():
     dO = torch.randn(*shp, p.d_v, device=dev, generator=g)
     eps = torch.tensor(0.5, device=dev)
     ws = onedf.Workspace(dev)
-    for _ in range(a.steps):
+    for _ in range(a.steps):            # the launches of bench.py's step
         qc, kc, _ = onedf.encode(p, Q, K, ws=ws)
         sc, pm = onedf.sort(p, kc, ws=ws)
-        O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws)
+        qo = onedf.query_schedule(p, qc, ws=ws)
+        O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws, qorder=qo)
         if not a.fwd_only:
-            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qcode=qc, perm=pm)
+            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qorder=qo, perm=pm)
     torch.cuda.synchronize()
     print("done", a.config)
 
