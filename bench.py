@@ -316,9 +316,25 @@ def run_gpu(args, cfg, world, rank, local):
     from paper_2501_14577_b200 import dist as odist
 
     bhs, (Bp, Hp) = rank_slices(cfg, world, rank, args.scaling)
-    x = _make_rank_inputs(cfg, bhs, (Bp, Hp))
-    t = {n: torch.from_numpy(v).to(dev) for n, v in x.items()}
+    if args.device_inputs:
+        # seeded N(0,1) inputs drawn on the device (shapes too large for the host recipe, e.g. long1m
+        # at B x H = 96: 51 GB); the synth/ recipe is what the parity tests use
+        import synth
+        g = torch.Generator(device=dev).manual_seed(synth.SEED_BASE + cfg.cfg_index + 1000 * rank)
+        x = None
+        t = {n: torch.randn(Bp, Hp, cfg.N, w, device=dev, generator=g)
+             for n, w in (("Q", cfg.d_k), ("K", cfg.d_k), ("V", cfg.d_v), ("dO", cfg.d_v))}
+    else:
+        x = _make_rank_inputs(cfg, bhs, (Bp, Hp))
+        t = {n: torch.from_numpy(v).to(dev) for n, v in x.items()}
     p = onedf.make_problem(**dict(cfg.problem_kwargs(), B=Bp, H=Hp))
+    # --groups G: the slices are processed in G contiguous groups (one workspace sized for a group,
+    # inputs and outputs of every slice resident) -- shapes whose workspace for all slices at once
+    # exceeds HBM (long1m at B x H = 96)
+    G = max(1, min(args.groups, Bp * Hp))
+    gsz = [(Bp * Hp) // G + (1 if g < (Bp * Hp) % G else 0) for g in range(G)]
+    gofs = [sum(gsz[:g]) for g in range(G)]
+    pg = [onedf.make_problem(**dict(cfg.problem_kwargs(), B=1, H=n)) for n in gsz]
     import synth
     eps = torch.tensor(synth.EPS, dtype=torch.float32, device=dev)
     N = cfg.N
@@ -331,8 +347,9 @@ def run_gpu(args, cfg, world, rank, local):
     idx = torch.empty((Bp, Hp, N, cfg.k), dtype=torch.int32, device=dev)
     Z = torch.empty((Bp, Hp, N), dtype=torch.float32, device=dev)
     dQ, dK, dV = torch.empty_like(t["Q"]), torch.empty_like(t["K"]), torch.empty_like(t["V"])
-    d_eps = torch.empty((), dtype=torch.float64, device=dev)
-    need = max(onedf.onedf_workspace_size(p, op) for op in (abi.OP_ENCODE, abi.OP_SORT, abi.OP_FWD, abi.OP_BWD))
+    d_eps = torch.empty((G,), dtype=torch.float64, device=dev)        # per group (summed by the consumer)
+    need = max(onedf.onedf_workspace_size(q, op) for q in pg for op in (abi.OP_ENCODE, abi.OP_SORT, abi.OP_FWD,
+                                                                         abi.OP_BWD))
     wsbuf = torch.empty(need + 256, dtype=torch.uint8, device=dev)
     ws = wsbuf.data_ptr() + ((-wsbuf.data_ptr()) % 256)
     wsbuf[(-wsbuf.data_ptr()) % 256:][:16].zero_()      # flag words (onedf.h "Errors")
@@ -343,25 +360,35 @@ def run_gpu(args, cfg, world, rank, local):
     NEV = 13
 
     def new_events():
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(NEV)]
-        for e in evs:
-            e.record(stream)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(NEV)] for _ in range(G)]
+        for ge in evs:
+            for e in ge:
+                e.record(stream)
         return evs
 
-    def step(ev):
-        ev[0].record(stream)
-        abi.onedf_encode(p, t["Q"], t["K"], None, qcode, kcode, None, ws, need, stream)
-        ev[1].record(stream)
-        abi.onedf_sort(p, kcode, scode, perm, ws, need, stream)
-        abi.onedf_sort(p, qcode, None, qorder, ws, need, stream)      # Morton query schedule for fwd and bwd
-        ev[2].record(stream)
-        abi.onedf_topk_attn_fwd_traced(p, t["Q"], t["K"], t["V"], eps, qcode, scode, perm, qorder, O, idx, Z, ws,
-                                       need, ev[3:6], stream)
-        abi.onedf_topk_attn_bwd_traced(p, t["Q"], t["K"], t["V"], eps, O, t["dO"], idx, Z, qcode, qorder, perm, dQ,
-                                       dK, dV, d_eps, ws, need, ev[6:12], stream)
-        if world > 1:
-            odist.combine_d_eps(d_eps)      # one f64 per rank, rank-ordered sum (D20)
-        ev[12].record(stream)
+    def ptr(tn, g, width=1):
+        return tn.data_ptr() + gofs[g] * N * width * tn.element_size()
+
+    def step(evg):
+        for g in range(G):
+            ev, q = evg[g], pg[g]
+            tq, tk, tv, tdo = (ptr(t[n], g, w) for n, w in (("Q", cfg.d_k), ("K", cfg.d_k), ("V", cfg.d_v),
+                                                             ("dO", cfg.d_v)))
+            qc, kc, sc, pm, qo = (ptr(a, g) for a in (qcode, kcode, scode, perm, qorder))
+            ev[0].record(stream)
+            abi.onedf_encode(q, tq, tk, None, qc, kc, None, ws, need, stream)
+            ev[1].record(stream)
+            abi.onedf_sort(q, kc, sc, pm, ws, need, stream)
+            abi.onedf_sort(q, qc, None, qo, ws, need, stream)      # Morton query schedule for fwd and bwd
+            ev[2].record(stream)
+            abi.onedf_topk_attn_fwd_traced(q, tq, tk, tv, eps, qc, sc, pm, qo, ptr(O, g, cfg.d_v), ptr(idx, g, cfg.k),
+                                           ptr(Z, g), ws, need, ev[3:6], stream)
+            abi.onedf_topk_attn_bwd_traced(q, tq, tk, tv, eps, ptr(O, g, cfg.d_v), tdo, ptr(idx, g, cfg.k), ptr(Z, g),
+                                           qc, qo, pm, ptr(dQ, g, cfg.d_k), ptr(dK, g, cfg.d_k), ptr(dV, g, cfg.d_v),
+                                           d_eps.data_ptr() + 8 * g, ws, need, ev[6:12], stream)
+            if world > 1 and G == 1:
+                odist.combine_d_eps(d_eps[0])   # one f64 per rank, rank-ordered sum (D20)
+            ev[12].record(stream)
 
     stage_names = ["encode", "sort", "fwd_means", "fwd_records", "fwd_topk", "bwd_means", "bwd_transpose",
                    "bwd_query", "bwd_key", "bwd_scans", "bwd_eps", "deps_exchange"]
@@ -398,9 +425,9 @@ def run_gpu(args, cfg, world, rank, local):
         clk = clocks.stop()
         total_ms = t0.elapsed_time(t1)
         stages = {n: [] for n in stage_names}
-        for ev in evs:
+        for evg in evs:
             for si, n in enumerate(stage_names):
-                stages[n].append(ev[si].elapsed_time(ev[si + 1]))
+                stages[n].append(sum(ev[si].elapsed_time(ev[si + 1]) for ev in evg))
         return total_ms, stages, clk
 
     total_ms, stages, clk = timed()
@@ -410,12 +437,12 @@ def run_gpu(args, cfg, world, rank, local):
     ms_rank = total_ms / args.steps
     ms = max_over_ranks(ms_rank, dev)
 
-    launches_per_step = count_launches(p)
+    launches_per_step = sum(count_launches(q) for q in pg)
     units = units_per_step(cfg, world, args.scaling)
 
     # ------------------------------------------------------------ e2e through the host-buffer entry point
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and x is not None:       # (device-drawn inputs have no host copy to stream)
         del O, idx, Z, dQ, dK, dV, wsbuf, qcode, kcode, scode, perm, qorder
         dev_inputs = t
         del dev_inputs, t
@@ -499,13 +526,18 @@ def run_gpu(args, cfg, world, rank, local):
 
 def count_launches(p) -> int:
     """Kernel launches of one step, from the library's launch plan (checked against the ncu launch
-    list in profiles/): encode 2 (bounds partials, encode), sort 2 (key runs, Morton query schedule
-    shared by fwd and bwd); fwd: prefix means 6 (mean slot), key records 1, top-k 1; bwd: prefix
-    means 6, CSR count + scan 2, query side 1, key side 1, mean-slot scans 6, eps 2."""
+    list in profiles/): encode 2 (bounds partials, encode); 2 sorts (key runs, Morton query
+    schedule shared by fwd and bwd), each 1 launch for runs <= 8192 keys else the onesweep's
+    histogram + bases + one launch per 8-bit digit; fwd: prefix means 6 (mean slot), key records 1,
+    top-k 1; bwd: prefix means 6, CSR count + scan 2, query side 1, long-segment order 1, key side
+    1, mean-slot scans 6, eps 2."""
     means = 6 if p.mean_slot else 0
+    run = p.N if not p.causal else min(p.chunk, p.N)
+    bits = p.d_k * (p.bits or min(63 // p.d_k, 32))
+    sort = 1 if run <= 8192 else 2 + (bits + 7) // 8
     fwd = means + 2
-    bwd = means + 2 + 1 + 1 + means + 2
-    return 2 + 2 + fwd + bwd
+    bwd = means + 2 + 1 + 1 + 1 + means + 2
+    return 2 + 2 * sort + fwd + bwd
 
 
 def _ncu_json(name):
@@ -553,6 +585,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--bh", type=int, default=0, help="override B x H with 1 x BH slices (config sweeps of long N)")
+    ap.add_argument("--groups", type=int, default=1, help="process the slices in G contiguous groups (one group's "
+                    "workspace; for shapes whose all-slice workspace exceeds HBM)")
+    ap.add_argument("--device-inputs", action="store_true", help="draw the seeded inputs on the device")
     args = ap.parse_args()
     world, rank, local = _dist_env()
     if args.gpus is not None and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
