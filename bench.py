@@ -529,14 +529,14 @@ def count_launches(p) -> int:
     list in profiles/): encode 2 (bounds partials, encode); 2 sorts (key runs, Morton query
     schedule shared by fwd and bwd), each 1 launch for runs <= 8192 keys else the onesweep's
     histogram + bases + one launch per 8-bit digit; fwd: prefix means 6 (mean slot), key records 1,
-    top-k 1; bwd: prefix means 6, CSR count + scan 2, query side 1, long-segment order 1, key side
-    1, mean-slot scans 6, eps 2."""
+    top-k 1; bwd: prefix means 6, CSR count 1 + offset scan 3 (block sums, their scan, apply),
+    query side 1, long-segment order 1, key side 1, mean-slot scans 6, eps 2."""
     means = 6 if p.mean_slot else 0
     run = p.N if not p.causal else min(p.chunk, p.N)
     bits = p.d_k * (p.bits or min(63 // p.d_k, 32))
     sort = 1 if run <= 8192 else 2 + (bits + 7) // 8
     fwd = means + 2
-    bwd = means + 2 + 1 + 1 + 1 + means + 2
+    bwd = means + 4 + 1 + 1 + 1 + means + 2
     return 2 + 2 * sort + fwd + bwd
 
 

@@ -8,7 +8,7 @@
 //       atomics: the counts, and everything derived from them, are exact and
 //       order-free);
 //   (2) exclusive scan per (b,h) -> CSR offsets off[j] (and the insertion
-//       cursors, a copy of off);
+//       cursors, a copy of off), multi-CTA;
 //   (3) the query side (bwd.cu K7) appends each record at
 //       atomicAdd(&cursor[j], 1) -- an integer slot, so only the ORDER inside
 //       a segment depends on scheduling, never a value;
@@ -25,6 +25,9 @@
 
 namespace onedf {
 
+constexpr int CSR_SCAN_THREADS = 256;
+constexpr int CSR_SB = CSR_SCAN_THREADS * 16;          // counts per block of the offset scan (2)
+
 void csr_carve(const onedf_problem* p, Carver* c, CsrBufs* t) {
     const int64_t BH = p->B * p->H, N = p->N, L = N * (int64_t)p->k;
     t->cursor = c->take<int32_t>((size_t)(BH * N));
@@ -34,6 +37,7 @@ void csr_carve(const onedf_problem* p, Carver* c, CsrBufs* t) {
     t->order = c->take<int32_t>((size_t)(BH * L));
     t->nlong = c->take<int32_t>(1);
     t->longseg = c->take<int2>((size_t)(BH * N));
+    t->bsum = c->take<int32_t>((size_t)(BH * ((N + CSR_SB - 1) / CSR_SB + 1)));
 }
 
 // (1) count.  A CTA takes CSR_QPC consecutive slots of the query schedule (the
@@ -86,49 +90,83 @@ __global__ void __launch_bounds__(CSR_THREADS) csr_count_kernel(const int32_t* _
     }
 }
 
-// (2) one CTA per (b,h): exclusive scan of cnt -> off[0..N] and cursor = off[0..N); every long
-// segment (csr_long_segment) is appended to the long-segment list
-constexpr int CSR_SCAN_THREADS = 1024;
-__global__ void __launch_bounds__(CSR_SCAN_THREADS) csr_scan_kernel(int32_t* __restrict__ cnt_cursor,
-                                                                    int32_t* __restrict__ off, int64_t N,
-                                                                    int32_t* __restrict__ nlong,
-                                                                    int2* __restrict__ longseg) {
-    __shared__ int32_t wsum[CSR_SCAN_THREADS / 32];
+// (2) exclusive scan of cnt -> off[0..N] and cursor = off[0..N) per (b,h), in three launches so a
+// long sequence is scanned by many CTAs: block sums of CSR_SB counts, a scan of the block sums per
+// (b,h), and the apply pass (integer arithmetic: exact whatever the order).  Every long segment
+// (csr_long_segment) is appended to the long-segment list.
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* s_w, int32_t& total) {
+    const int lane = lane_id(), w = threadIdx.x / 32, nw = blockDim.x / 32;
+    int32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    int32_t woff = 0, tot = 0;
+    for (int x = 0; x < nw; ++x) {
+        woff += x < w ? s_w[x] : 0;
+        tot += s_w[x];
+    }
+    __syncthreads();
+    total = tot;
+    return woff + inc - v;
+}
+
+__global__ void __launch_bounds__(CSR_SCAN_THREADS) csr_blocksum_kernel(const int32_t* __restrict__ cnt, int64_t N,
+                                                                        int32_t* __restrict__ bsum, int64_t nblk) {
+    __shared__ int32_t s_w[CSR_SCAN_THREADS / 32];
+    const int64_t bh = blockIdx.y, b0 = (int64_t)blockIdx.x * CSR_SB;
+    int32_t sum = 0;
+    for (int64_t t = b0 + threadIdx.x; t < min64(N, b0 + CSR_SB); t += CSR_SCAN_THREADS) sum += cnt[bh * N + t];
+    int32_t total;
+    block_excl_scan(sum, s_w, total);
+    if (threadIdx.x == 0) bsum[bh * (nblk + 1) + blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(CSR_SCAN_THREADS) csr_blockscan_kernel(int32_t* __restrict__ bsum, int64_t nblk,
+                                                                         int32_t* __restrict__ off, int64_t N) {
+    __shared__ int32_t s_w[CSR_SCAN_THREADS / 32];
     const int64_t bh = blockIdx.x;
+    int32_t* b = bsum + bh * (nblk + 1);
+    const int64_t per = (nblk + CSR_SCAN_THREADS - 1) / CSR_SCAN_THREADS;
+    const int64_t u0 = min64(nblk, (int64_t)threadIdx.x * per), u1 = min64(nblk, u0 + per);
+    int32_t sum = 0;
+    for (int64_t u = u0; u < u1; ++u) sum += b[u];
+    int32_t total;
+    int32_t run = block_excl_scan(sum, s_w, total);
+    for (int64_t u = u0; u < u1; ++u) { const int32_t x = b[u]; b[u] = run; run += x; }
+    if (threadIdx.x == 0) off[bh * (N + 1) + N] = total;
+}
+
+__global__ void __launch_bounds__(CSR_SCAN_THREADS) csr_apply_kernel(int32_t* __restrict__ cnt_cursor,
+                                                                     int32_t* __restrict__ off, int64_t N,
+                                                                     const int32_t* __restrict__ bsum, int64_t nblk,
+                                                                     int32_t* __restrict__ nlong,
+                                                                     int2* __restrict__ longseg) {
+    __shared__ int32_t s_w[CSR_SCAN_THREADS / 32];
+    const int64_t bh = blockIdx.y, b0 = (int64_t)blockIdx.x * CSR_SB;
     int32_t* c = cnt_cursor + bh * N;
     int32_t* o = off + bh * (N + 1);
-    const int64_t per = (N + CSR_SCAN_THREADS - 1) / CSR_SCAN_THREADS;
-    const int64_t a0 = (int64_t)threadIdx.x * per, a1 = min64(N, a0 + per);
+    constexpr int PER = CSR_SB / CSR_SCAN_THREADS;       // contiguous counts per thread
+    const int64_t a0 = b0 + (int64_t)threadIdx.x * PER, a1 = min64(N, a0 + PER);
+    int32_t v[PER];
     int32_t sum = 0;
-    for (int64_t t = a0; t < a1; ++t) sum += c[t];
-    const int lane = lane_id(), w = threadIdx.x / 32;
-    int32_t inc = sum;
 #pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-        const int32_t y = __shfl_up_sync(FULL, inc, s);
-        if (lane >= s) inc += y;
+    for (int u = 0; u < PER; ++u) {
+        v[u] = a0 + u < a1 ? c[a0 + u] : 0;
+        sum += v[u];
     }
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {
-        const int32_t v = wsum[lane];
-        int32_t x = v;
+    int32_t total;
+    int32_t run = bsum[bh * (nblk + 1) + blockIdx.x] + block_excl_scan(sum, s_w, total);
 #pragma unroll
-        for (int s = 1; s < 32; s <<= 1) {
-            const int32_t y = __shfl_up_sync(FULL, x, s);
-            if (lane >= s) x += y;
-        }
-        wsum[lane] = x - v;
-        if (lane == 31) o[N] = x;
-    }
-    __syncthreads();
-    int32_t run = wsum[w] + inc - sum;
-    for (int64_t t = a0; t < a1; ++t) {
-        const int32_t x = c[t];
-        o[t] = run;
-        c[t] = run;                                               // insertion cursor
-        run += x;
-        if (x > 0 && csr_long_segment(x, N)) longseg[atomicAdd(nlong, 1)] = make_int2((int)bh, (int)t);
+    for (int u = 0; u < PER; ++u) {
+        if (a0 + u >= a1) break;
+        o[a0 + u] = run;
+        c[a0 + u] = run;                                           // insertion cursor
+        if (v[u] > 0 && csr_long_segment(v[u], N)) longseg[atomicAdd(nlong, 1)] = make_int2((int)bh, (int)(a0 + u));
+        run += v[u];
     }
 }
 
@@ -288,7 +326,11 @@ cudaError_t launch_csr_count(const onedf_problem* p, const int32_t* idx, const i
         const dim3 grid((unsigned)((nq + CSR_QPC - 1) / CSR_QPC), (unsigned)BH);
         csr_count_kernel<<<grid, CSR_THREADS, 0, st>>>(idx, qorder, N, nq, p->k, sh, t->cursor);
     }
-    csr_scan_kernel<<<(unsigned)BH, CSR_SCAN_THREADS, 0, st>>>(t->cursor, t->offsets, N, t->nlong, t->longseg);
+    const int64_t nblk = (N + CSR_SB - 1) / CSR_SB;
+    const dim3 gb((unsigned)nblk, (unsigned)BH);
+    csr_blocksum_kernel<<<gb, CSR_SCAN_THREADS, 0, st>>>(t->cursor, N, t->bsum, nblk);
+    csr_blockscan_kernel<<<(unsigned)BH, CSR_SCAN_THREADS, 0, st>>>(t->bsum, nblk, t->offsets, N);
+    csr_apply_kernel<<<gb, CSR_SCAN_THREADS, 0, st>>>(t->cursor, t->offsets, N, t->bsum, nblk, t->nlong, t->longseg);
     return cudaGetLastError();
 }
 

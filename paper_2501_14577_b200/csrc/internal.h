@@ -76,6 +76,7 @@ struct CsrBufs {
     int32_t* order;     // [BH][N*k]  ascending-i order of the long segments (csr_long_segment)
     int32_t* nlong;     // [1]        number of long segments
     int2* longseg;      // [BH*N]     their (bh, j), in no particular order (each is ordered independently)
+    int32_t* bsum;      // [BH][N/4096 + 1] block sums of the multi-CTA offset scan
 };
 void csr_carve(const onedf_problem* p, Carver* c, CsrBufs* t);
 // qorder: the query schedule (nullable -> natural order); only its grouping of similar queries matters

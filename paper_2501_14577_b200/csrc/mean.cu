@@ -125,19 +125,42 @@ __global__ void __launch_bounds__(SCAN_THREADS) scan_tile_sums_kernel(const Scan
 }
 
 // (2) per (bh, column): exclusive scan over tiles (forward) or suffix scan
-// (reverse); part[ntile] = total.
-__global__ void scan_tiles_kernel(double* __restrict__ part, int64_t ntile, int C, int reverse) {
+// (reverse); part[ntile] = total.  One CTA per (bh, column): every thread sums a
+// contiguous stretch of tiles, a fixed warp/CTA scan combines the stretches, then
+// every thread rewrites its stretch -- a fixed combination order (deterministic),
+// and no serial walk over the ntile = N/256 tiles of a long sequence.
+constexpr int TSCAN_THREADS = 256;
+__global__ void __launch_bounds__(TSCAN_THREADS) scan_tiles_kernel(double* __restrict__ part, int64_t ntile, int C,
+                                                                   int reverse) {
+    __shared__ double s_w[TSCAN_THREADS / 32];
     const int64_t bh = blockIdx.x;
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-        double run = 0.0;
-        for (int64_t u = 0; u < ntile; ++u) {
-            const int64_t b = reverse ? ntile - 1 - u : u;
-            double* x = part + (bh * (ntile + 1) + b) * C + c;
-            const double t = *x;
-            *x = run;
-            run += t;
-        }
-        part[(bh * (ntile + 1) + ntile) * C + c] = run;
+    const int c = blockIdx.y;
+    const int64_t per = (ntile + TSCAN_THREADS - 1) / TSCAN_THREADS;
+    const int64_t u0 = min64(ntile, (int64_t)threadIdx.x * per), u1 = min64(ntile, u0 + per);
+    auto at = [&](int64_t u) -> double* {                 // u-th tile in scan order
+        const int64_t b = reverse ? ntile - 1 - u : u;
+        return part + (bh * (ntile + 1) + b) * C + c;
+    };
+    double sum = 0.0;
+    for (int64_t u = u0; u < u1; ++u) sum += *at(u);
+    const int lane = lane_id(), w = threadIdx.x / 32;
+    double inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    double woff = 0.0;
+    for (int x = 0; x < w; ++x) woff += s_w[x];
+    double run = woff + (inc - sum);                       // exclusive prefix of this stretch
+    if (threadIdx.x == TSCAN_THREADS - 1) part[(bh * (ntile + 1) + ntile) * C + c] = woff + inc;
+    for (int64_t u = u0; u < u1; ++u) {
+        double* x = at(u);
+        const double t = *x;
+        *x = run;
+        run += t;
     }
 }
 
@@ -252,8 +275,8 @@ cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const vo
     const int cwk = pow2_at_least(p->d_k), cwv = pow2_at_least(p->d_v);
     scan_tile_sums_kernel<0, float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
     ONEDF_DISPATCH_TV(p->vdtype, { scan_tile_sums_kernel<0, TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV); });
-    scan_tiles_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, 0);
-    scan_tiles_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, 0);
+    scan_tiles_kernel<<<dim3((unsigned)BH, (unsigned)p->d_k), TSCAN_THREADS, 0, st>>>(partK, nt, p->d_k, 0);
+    scan_tiles_kernel<<<dim3((unsigned)BH, (unsigned)p->d_v), TSCAN_THREADS, 0, st>>>(partV, nt, p->d_v, 0);
     if (p->causal) {
         mean_apply_kernel<float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, m->Kbar);
         ONEDF_DISPATCH_TV(p->vdtype, { mean_apply_kernel<TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, m->Vbar); });
@@ -276,8 +299,8 @@ cudaError_t launch_mean_grad_scan(const onedf_problem* p, const float* Q, const 
     const int cwk = pow2_at_least(p->d_k), cwv = pow2_at_least(p->d_v);
     scan_tile_sums_kernel<1, float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK);
     ONEDF_DISPATCH_TV(p->vdtype, { scan_tile_sums_kernel<2, TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV); });
-    scan_tiles_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, 1);
-    scan_tiles_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, 1);
+    scan_tiles_kernel<<<dim3((unsigned)BH, (unsigned)p->d_k), TSCAN_THREADS, 0, st>>>(partK, nt, p->d_k, 1);
+    scan_tiles_kernel<<<dim3((unsigned)BH, (unsigned)p->d_v), TSCAN_THREADS, 0, st>>>(partV, nt, p->d_v, 1);
     grad_apply_kernel<1, float, float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, dK, dK);
     ONEDF_DISPATCH_TV(p->vdtype, {
         grad_apply_kernel<2, TV, TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, dV32, static_cast<TV*>(dV));

@@ -176,6 +176,7 @@ struct OsArgs {
     const uint64_t* kcode; uint64_t* scode; int32_t* perm;
     SortScratch scr;
     int64_t N, M, runs_per_bh, tiles;   // tiles per run (uniform; a short last run has empty tiles)
+    Shard sh;                            // sharded: other ranks' runs arrive by all-gather (skipped)
 };
 
 // (0) digit counts of every pass, per run
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(OS_THREADS) os_hist_kernel(const OsArgs a, int
     __syncthreads();
     const int64_t run = blockIdx.x / a.tiles, tile = blockIdx.x % a.tiles;
     const int64_t bh = run / a.runs_per_bh, c = run % a.runs_per_bh;
+    if (a.sh.on() && Shard::owner(c, a.sh.world) != a.sh.rank) return;
     const int64_t s0 = c * a.M, n = min64(a.M, a.N - s0);
     const uint64_t* src = a.kcode + bh * a.N + s0;
     for (int64_t r = tile * OS_TILE + threadIdx.x; r < min64(n, (tile + 1) * OS_TILE); r += OS_THREADS) {
@@ -221,6 +223,8 @@ __global__ void __launch_bounds__(OS_THREADS) os_pass_kernel(const OsArgs a, int
     const int64_t tid = s_ticket;
     const int64_t run = tid / a.tiles, tile = tid % a.tiles;
     const int64_t bh = run / a.runs_per_bh, c = run % a.runs_per_bh;
+    // sharded: the whole run is skipped (only later tiles of the same run look back at its tiles)
+    if (a.sh.on() && Shard::owner(c, a.sh.world) != a.sh.rank) return;
     const int64_t s0 = c * a.M, n = min64(a.M, a.N - s0);
     const int64_t r0 = tile * OS_TILE;
     const int nt = (int)max((int64_t)0, min64(OS_TILE, n - r0));
@@ -322,6 +326,7 @@ static cudaError_t launch_onesweep(const onedf_problem* p, const uint64_t* kcode
     OsArgs a;
     a.kcode = kcode; a.scode = scode; a.perm = perm; a.scr = scr;
     a.N = p->N; a.M = run_len_max(p); a.runs_per_bh = num_runs(p); a.tiles = os_tiles(p);
+    a.sh = make_shard(p);
     const int64_t runs = p->B * p->H * a.runs_per_bh;
     const int passes = os_passes(p);
     cudaError_t e = cudaMemsetAsync(scr.base, 0, (size_t)runs * 8 * 256 * 4, st);
