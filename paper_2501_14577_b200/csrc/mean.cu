@@ -67,6 +67,7 @@ __device__ __forceinline__ double scan_value(const ScanSrc& s, int64_t bh, int64
     const float2 mc = __ldg(s.muco + row);
     double y;
     if (MODE == 1) {
+        if (mc.y == 0.f) return 0.0;      // no mean-slot weight (e.g. another rank's query: Kbar unwritten)
         const float kb = __ldg(s.Kbar + (bh * (s.causal ? N : 1) + (s.causal ? i : 0)) * s.C + c);
         y = (double)mc.y * (xval<TX>(s, row * s.C + c) - s.kt * (double)kb);
     } else {
@@ -168,10 +169,17 @@ __global__ void __launch_bounds__(TSCAN_THREADS) scan_tiles_kernel(double* __res
 template <typename TX>
 __global__ void __launch_bounds__(SCAN_THREADS) mean_apply_kernel(const ScanSrc s, int64_t N, int64_t ntile, int CW,
                                                                   const double* __restrict__ part,
-                                                                  float* __restrict__ out) {
+                                                                  float* __restrict__ out, Shard shd) {
     __shared__ double sh[SCAN_THREADS];
     __shared__ double s_inv[SCAN_TB];
     const int64_t bh = blockIdx.y, tile = blockIdx.x;
+    // sharded: the means are read only at this rank's query rows -- skip tiles with none of them
+    if (shd.on()) {
+        const int64_t r0 = tile * SCAN_TB, r1 = min64(N, r0 + SCAN_TB) - 1;
+        bool any = false;
+        for (int64_t c = r0 / shd.M; c <= r1 / shd.M && !any; ++c) any = Shard::owner(c, shd.world) == shd.rank;
+        if (!any) return;
+    }
     const int c = threadIdx.x % CW, g = threadIdx.x / CW, RG = SCAN_THREADS / CW;
     const int per = SCAN_TB / RG;
     const int64_t r0 = tile * SCAN_TB + (int64_t)g * per, r1 = min64(N, r0 + per);
@@ -278,8 +286,11 @@ cudaError_t launch_prefix_means(const onedf_problem* p, const float* K, const vo
     scan_tiles_kernel<<<dim3((unsigned)BH, (unsigned)p->d_k), TSCAN_THREADS, 0, st>>>(partK, nt, p->d_k, 0);
     scan_tiles_kernel<<<dim3((unsigned)BH, (unsigned)p->d_v), TSCAN_THREADS, 0, st>>>(partV, nt, p->d_v, 0);
     if (p->causal) {
-        mean_apply_kernel<float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, m->Kbar);
-        ONEDF_DISPATCH_TV(p->vdtype, { mean_apply_kernel<TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, m->Vbar); });
+        const Shard shd = make_shard(p);
+        mean_apply_kernel<float><<<grid, SCAN_THREADS, 0, st>>>(sk, N, nt, cwk, partK, m->Kbar, shd);
+        ONEDF_DISPATCH_TV(p->vdtype, {
+            mean_apply_kernel<TV><<<grid, SCAN_THREADS, 0, st>>>(sv, N, nt, cwv, partV, m->Vbar, shd);
+        });
     } else {
         mean_global_kernel<<<(unsigned)BH, 32, 0, st>>>(partK, nt, p->d_k, N, m->Kbar);
         mean_global_kernel<<<(unsigned)BH, 256, 0, st>>>(partV, nt, p->d_v, N, m->Vbar);

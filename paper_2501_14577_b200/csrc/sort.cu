@@ -200,13 +200,24 @@ __global__ void __launch_bounds__(OS_THREADS) os_hist_kernel(const OsArgs a, int
     }
 }
 
-// counts -> exclusive digit bases, one thread per (run, pass)
+// counts -> exclusive digit bases, one warp per (run, pass): 8 digits per lane + a warp scan
 __global__ void os_base_kernel(const OsArgs a, int64_t runs, int passes) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
     if (t >= runs * passes) return;
-    uint32_t* b = a.scr.base + (t / passes) * 8 * 256 + (t % passes) * 256;
-    uint32_t run = 0;
-    for (int d = 0; d < 256; ++d) { const uint32_t x = b[d]; b[d] = run; run += x; }
+    const int lane = lane_id();
+    uint32_t* b = a.scr.base + (t / passes) * 8 * 256 + (t % passes) * 256 + lane * 8;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) { v[d] = b[d]; sum += v[d]; }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int d = 0; d < 8; ++d) { b[d] = run; run += v[d]; }
 }
 
 // one digit pass over one tile (the ticket decides which)
@@ -337,7 +348,7 @@ static cudaError_t launch_onesweep(const onedf_problem* p, const uint64_t* kcode
     e = cudaFuncSetAttribute(os_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     os_hist_kernel<<<grid, OS_THREADS, 0, st>>>(a, passes);
-    os_base_kernel<<<(unsigned)((runs * passes + 255) / 256), 256, 0, st>>>(a, runs, passes);
+    os_base_kernel<<<(unsigned)((runs * passes * 32 + 255) / 256), 256, 0, st>>>(a, runs, passes);
     for (int ps = 0; ps < passes; ++ps) {
         e = cudaMemsetAsync(scr.status, 0, (size_t)runs * a.tiles * 256 * 4, st);
         if (e != cudaSuccess) return e;
