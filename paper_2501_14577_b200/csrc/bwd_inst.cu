@@ -39,14 +39,21 @@ void launch_bwd_query_dk(const BwdArgs& a, int P, int nch, int dv, int k, unsign
     else bwd_query_launch_r<DK, TV, 32>(a, nch, dv, k, grid, st);
 }
 
+// WHOLE: d_v == 4*P*CH (every lane chunk exists; d_v a compile-time constant in the gathers)
+template <int DK, typename TV, int PV, int CHV>
+static void bwd_key_launch(const KeyArgs& ka, int dv, unsigned grid, cudaStream_t st) {
+    if (4 * PV * CHV == dv) bwd_key_kernel<DK, PV, CHV, true, TV><<<grid, BWD_THREADS, 0, st>>>(ka);
+    else bwd_key_kernel<DK, PV, CHV, false, TV><<<grid, BWD_THREADS, 0, st>>>(ka);
+}
+
 template <int DK, typename TV>
 void launch_bwd_key_dk(const KeyArgs& ka, int P, int dv, unsigned grid, cudaStream_t st) {
     if (!grid) return;
-    if (P == 4) bwd_key_kernel<DK, 4, 1, TV><<<grid, BWD_THREADS, 0, st>>>(ka);
-    else if (P == 8) bwd_key_kernel<DK, 8, 1, TV><<<grid, BWD_THREADS, 0, st>>>(ka);
-    else if (P == 16) bwd_key_kernel<DK, 16, 1, TV><<<grid, BWD_THREADS, 0, st>>>(ka);
-    else if (dv > 128) bwd_key_kernel<DK, 32, 2, TV><<<grid, BWD_THREADS, 0, st>>>(ka);
-    else bwd_key_kernel<DK, 32, 1, TV><<<grid, BWD_THREADS, 0, st>>>(ka);
+    if (P == 4) bwd_key_launch<DK, TV, 4, 1>(ka, dv, grid, st);
+    else if (P == 8) bwd_key_launch<DK, TV, 8, 1>(ka, dv, grid, st);
+    else if (P == 16) bwd_key_launch<DK, TV, 16, 1>(ka, dv, grid, st);
+    else if (dv > 128) bwd_key_launch<DK, TV, 32, 2>(ka, dv, grid, st);
+    else bwd_key_launch<DK, TV, 32, 1>(ka, dv, grid, st);
 }
 
 template void launch_bwd_query_dk<ONEDF_INST_DK_A, ONEDF_INST_TV>(const BwdArgs&, int, int, int, int, unsigned,

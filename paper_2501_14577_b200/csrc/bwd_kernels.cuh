@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
     }
     const int64_t mrow = a.causal ? i : 0;
     const TV* Vb = static_cast<const TV*>(a.V) + bh * N * (int64_t)dv;
+    const TV* Vl = Vb + 4 * l;                    // this lane's first chunk of row 0
     const int owner_t = l >> (LOGP - LOGT);
     const bool owner = (l & ((1 << (LOGP - LOGT)) - 1)) == 0;
     double* sp = s_part[warp];
@@ -142,11 +143,17 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_query_kernel(
             for (int t = 0; t < T; ++t) {
                 const int j = __shfl_sync(FULL, jr[r], (h0 + t * G + grp) & 31);
                 // an unselected slot (j < 0) reads row 0; its dot is never used (phase 2 skips it)
-                const TV* vr = Vb + (int64_t)(j < 0 ? 0 : j) * dv;
+                const int jj = j < 0 ? 0 : j;
+                if (WHOLE) {
+                    // P*CH == d_v/4: d_v is a constant and every chunk exists; lane base + row offset
+                    const TV* vr = Vl + (int64_t)jj * (4 * P * CH);
 #pragma unroll
-                for (int h = 0; h < CH; ++h) {
-                    if (WHOLE) x[t][h] = ld4(vr, l + h * P);            // P*CH == d_v/4: every chunk exists
-                    else x[t][h] = l + h * P < nch ? ld4(vr, l + h * P) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int h = 0; h < CH; ++h) x[t][h] = ld4(vr, h * P);
+                } else {
+                    const TV* vr = Vb + (int64_t)jj * dv;
+#pragma unroll
+                    for (int h = 0; h < CH; ++h)
+                        x[t][h] = l + h * P < nch ? ld4(vr, l + h * P) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
 #pragma unroll
@@ -303,7 +310,7 @@ __device__ __forceinline__ void sort_prefix(uint32_t (&x)[8]) {
     for (int r = 0; r < R; ++r) x[r] = y[r];
 }
 
-template <int DK, int P, int CH, typename TV>
+template <int DK, int P, int CH, bool WHOLE, typename TV>
 __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(const KeyArgs a) {
     constexpr int G = 32 / P;
     constexpr int U = ONEDF_KEY_U;                // entries per lane group in flight
@@ -364,6 +371,7 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[h][c] = 0.0;
     const TV* dOb = static_cast<const TV*>(a.dO) + bh * N * (int64_t)dv;
+    const TV* dOl = dOb + 4 * l;                  // this lane's first chunk of row 0
     const float* Qb = a.Q + bh * N * DK;
 
     for (int32_t b0 = 0; b0 < len; b0 += 32) {
@@ -391,17 +399,30 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
         for (int t0 = 0; t0 < n; t0 += G * U) {
             float4 x[U][CH];
             float Au[U];
+            if (WHOLE && t0 + G * U <= n) {
+                // d_v = 4*P*CH and all U entries of every group present: lane base + row offset, no masks
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int src = t0 + u * G + grp;
-                const int iu = __shfl_sync(FULL, iq, src & 31);
-                Au[u] = __shfl_sync(FULL, aw.x, src & 31);
-                const bool ok = src < n;
-                if (!ok) Au[u] = 0.f;
+                for (int u = 0; u < U; ++u) {
+                    const int src = t0 + u * G + grp;
+                    const int iu = __shfl_sync(FULL, iq, src);
+                    Au[u] = __shfl_sync(FULL, aw.x, src);
+                    const TV* rp = dOl + (int64_t)iu * (4 * P * CH);
 #pragma unroll
-                for (int h = 0; h < CH; ++h) {
-                    const int ch = l + h * P;
-                    x[u][h] = (ok && ch < nch) ? ld4(dOb + (int64_t)iu * dv, ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int h = 0; h < CH; ++h) x[u][h] = ld4(rp, h * P);
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int src = t0 + u * G + grp;
+                    const int iu = __shfl_sync(FULL, iq, src & 31);
+                    Au[u] = __shfl_sync(FULL, aw.x, src & 31);
+                    const bool ok = src < n;
+                    if (!ok) Au[u] = 0.f;
+#pragma unroll
+                    for (int h = 0; h < CH; ++h) {
+                        const int ch = l + h * P;
+                        x[u][h] = (ok && ch < nch) ? ld4(dOb + (int64_t)iu * dv, ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
                 }
             }
             // the U = 4 entries summed in f32 (sum4, fixed order), promoted once per value (reading R5)
