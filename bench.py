@@ -490,8 +490,8 @@ def run_gpu(args, cfg, world, rank, local):
     avg = {n: sum(v) / len(v) for n, v in stages.items()}
     dom = max(kern_map, key=lambda n: avg[n])
     achieved = ab[kern_map[dom]] / (avg[dom] / 1e3) / 1e9
-    traffic = _ncu_traffic(dom, cfg.name) if (Bp, Hp) == (cfg.B, cfg.H) else None
-    step_dram = _ncu_step_dram(cfg.name) if (Bp, Hp) == (cfg.B, cfg.H) else None
+    traffic = _ncu_traffic(dom, cfg.name) if Bp * Hp == cfg.BH else None
+    step_dram = _ncu_step_dram(cfg.name) if Bp * Hp == cfg.BH else None
     roof = {"bound": "hbm", "kernel": {"fwd_topk": "topk_attn_fwd_kernel", "bwd_query": "bwd_query_kernel",
                                        "bwd_key": "bwd_key_kernel"}[dom],
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

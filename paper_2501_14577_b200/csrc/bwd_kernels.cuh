@@ -426,13 +426,25 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
                 }
             }
             // the U = 4 entries summed in f32 (sum4, fixed order), promoted once per value (reading R5)
-            static_assert(U == 4, "the f32 group of the dV gather is 4 entries");
+            // each group of 4 entries (u = 4m .. 4m+3: entries t0 + 8m .. t0 + 8m + 7 of the chunk) is
+            // summed in f32 (sum4, fixed order) and promoted once per value (reading R5); groups in
+            // ascending entry order, a group past the chunk's last entry skipped -- the same sums
+            // in the same order for any U
+            static_assert(U % 4 == 0, "the f32 group of the dV gather is 4 entries");
 #pragma unroll
-            for (int h = 0; h < CH; ++h) {
-                acc[h][0] += (double)sum4(Au[0], x[0][h].x, Au[1], x[1][h].x, Au[2], x[2][h].x, Au[3], x[3][h].x);
-                acc[h][1] += (double)sum4(Au[0], x[0][h].y, Au[1], x[1][h].y, Au[2], x[2][h].y, Au[3], x[3][h].y);
-                acc[h][2] += (double)sum4(Au[0], x[0][h].z, Au[1], x[1][h].z, Au[2], x[2][h].z, Au[3], x[3][h].z);
-                acc[h][3] += (double)sum4(Au[0], x[0][h].w, Au[1], x[1][h].w, Au[2], x[2][h].w, Au[3], x[3][h].w);
+            for (int m = 0; m < U; m += 4) {
+                if (m > 0 && t0 + m * G >= n) break;
+#pragma unroll
+                for (int h = 0; h < CH; ++h) {
+                    acc[h][0] += (double)sum4(Au[m], x[m][h].x, Au[m + 1], x[m + 1][h].x, Au[m + 2], x[m + 2][h].x,
+                                              Au[m + 3], x[m + 3][h].x);
+                    acc[h][1] += (double)sum4(Au[m], x[m][h].y, Au[m + 1], x[m + 1][h].y, Au[m + 2], x[m + 2][h].y,
+                                              Au[m + 3], x[m + 3][h].y);
+                    acc[h][2] += (double)sum4(Au[m], x[m][h].z, Au[m + 1], x[m + 1][h].z, Au[m + 2], x[m + 2][h].z,
+                                              Au[m + 3], x[m + 3][h].z);
+                    acc[h][3] += (double)sum4(Au[m], x[m][h].w, Au[m + 1], x[m + 1][h].w, Au[m + 2], x[m + 2][h].w,
+                                              Au[m + 3], x[m + 3][h].w);
+                }
             }
         }
         // dK: the lane owning the entry, f64, fixed entry -> lane map

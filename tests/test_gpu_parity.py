@@ -117,6 +117,41 @@ def test_eps_values():
 
 
 # ------------------------------------------------------------------ BASELINE.json configs
+# the grouped selection of repeated keys (fwd_kernels.cuh select_groups): many equal distances
+# collected (cnt > 128, ties among the first sorted keys) or more than FWD_CAP at or below T; k
+# spans R = 1, 2, 4 register rows; "mirror" puts distinct key rows at exactly equal distance from
+# queries at the origin (two groups of equal D in one run -> the streaming fallback); every
+# result bit-exact / within tolerance of the oracle
+TIE_CASES = {
+    "k16_causal": (dict(B=1, H=2, N=2048, d_k=3, d_v=16, k=16, window=64, chunk=128, causal=1, mean_slot=1), 5),
+    "k64_causal": (dict(B=1, H=2, N=4096, d_k=3, d_v=64, k=64, window=128, chunk=256, causal=1, mean_slot=1), 9),
+    "k100_causal": (dict(B=1, H=1, N=4096, d_k=3, d_v=8, k=100, window=160, chunk=512, causal=1, mean_slot=1), 6),
+    "k64_noncausal": (dict(B=1, H=1, N=2048, d_k=3, d_v=8, k=64, window=128, chunk=1, causal=0, mean_slot=1), 9),
+    "k64_mirror": (dict(B=1, H=1, N=2048, d_k=3, d_v=8, k=64, window=128, chunk=256, causal=1, mean_slot=1), -4),
+}
+
+
+@pytest.mark.parametrize("name", list(TIE_CASES))
+def test_repeated_keys_grouped_selection(name):
+    kw, vocab = TIE_CASES[name]
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    B, H, N, dk = kw["B"], kw["H"], kw["N"], kw["d_k"]
+    x = _rand_inputs(kw, seed=zlib.crc32(name.encode()) % 1000)
+    if vocab > 0:
+        emb = rng.normal(size=(vocab, dk)).astype(np.float32)
+        tok = rng.integers(0, vocab, size=(B, H, N))
+        x["K"] = emb[tok]
+        x["Q"] = (emb[tok] + 0.05 * rng.normal(size=(B, H, N, dk))).astype(np.float32)
+    else:
+        v = rng.normal(size=(-vocab, dk)).astype(np.float32)
+        emb = np.concatenate([v, -v])                     # +v and -v: equal distance from the origin
+        tok = rng.integers(0, len(emb), size=(B, H, N))
+        x["K"] = emb[tok]
+        x["Q"] = (0.3 * rng.normal(size=(B, H, N, dk))).astype(np.float32)
+        x["Q"][:, :, ::3] = 0.0                           # every third query at the origin
+    _compare_all(gpu_run(kw, x), oracle_run(kw, x))
+
+
 CONFIG_NAMES = ["ar", "ar_tokens", "lra_nc", "lra_c", "lra_tokens", "wiki", "wiki_tokens"]
 
 

@@ -13,16 +13,21 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="long64k")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--bwd", action="store_true")
+ap.add_argument("--synth", action="store_true", help="the config's seeded synth/ inputs (e.g. tokens) instead of iid")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
 p = onedf.make_problem(**cfg.problem_kwargs())
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(1)
 shp = (p.B, p.H, p.N)
-Q = torch.randn(*shp, p.d_k, device=dev, generator=g)
-K = torch.randn(*shp, p.d_k, device=dev, generator=g)
-V = torch.randn(*shp, p.d_v, device=dev, generator=g)
-dO = torch.randn(*shp, p.d_v, device=dev, generator=g)
+if a.synth:
+    x = synth.make_inputs(cfg)
+    Q, K, V, dO = (torch.from_numpy(x[n]).to(dev) for n in ("Q", "K", "V", "dO"))
+else:
+    Q = torch.randn(*shp, p.d_k, device=dev, generator=g)
+    K = torch.randn(*shp, p.d_k, device=dev, generator=g)
+    V = torch.randn(*shp, p.d_v, device=dev, generator=g)
+    dO = torch.randn(*shp, p.d_v, device=dev, generator=g)
 eps = torch.tensor(0.5, device=dev)
 ws = onedf.Workspace(dev)
 qc, kc, _ = onedf.encode(p, Q, K, ws=ws)
