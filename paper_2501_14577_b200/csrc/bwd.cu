@@ -26,7 +26,7 @@
 // key's CSR segment (integer cursor, csr.cu).
 // K9: one warp per key j (keys visited in sorted-run order when perm is
 // given) orders its CSR segment by query position (register bitonic sort of
-// (i << 8 | position) keys up to 256 entries; longer segments were ordered by
+// (i << 9 | position) keys up to KEY_REG_SEG = 512 entries; longer segments were ordered by
 // csr.cu's bitmap counting sort after the query side), then
 // walks it 32 entries at a time: lane groups of P gather the dO_i rows into
 // f64 accumulators, a fixed shuffle tree at the end -- a deterministic

@@ -301,7 +301,7 @@ struct KeyArgs {
 
 
 template <int R>
-__device__ __forceinline__ void sort_prefix(uint32_t (&x)[8]) {
+__device__ __forceinline__ void sort_prefix(uint32_t (&x)[KEY_REG_SEG / 32]) {
     uint32_t y[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) y[r] = x[r];
@@ -339,21 +339,22 @@ __global__ void __launch_bounds__(BWD_THREADS, ONEDF_BWD_MINB) bwd_key_kernel(co
 
     // ---- fixed visiting order: ascending query position i (distinct within a segment)
     const bool small = !csr_long_segment(len, N);
-    uint32_t* sk = s_key[warp];                   // sorted (i << 8 | position) keys
+    uint32_t* sk = s_key[warp];                   // sorted (i << KEY_POS_BITS | position) keys
     const int32_t* go = a.order + bh * a.L + s0;
     if (small) {
-        uint32_t xs[8];
+        uint32_t xs[KEY_REG_SEG / 32];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < KEY_REG_SEG / 32; ++r) {
             const int e = r * 32 + lane;
             xs[r] = e < len ? ((uint32_t)__ldg(ri + e) << KEY_POS_BITS) | (uint32_t)e : ~0u;
         }
         if (len <= 32) sort_prefix<1>(xs);
         else if (len <= 64) sort_prefix<2>(xs);
         else if (len <= 128) sort_prefix<4>(xs);
-        else sort_prefix<8>(xs);
+        else if (KEY_REG_SEG <= 256 || len <= 256) sort_prefix<8>(xs);
+        else sort_prefix<(KEY_REG_SEG > 256 ? 16 : 8)>(xs);
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < KEY_REG_SEG / 32; ++r)
             if (r * 32 < len) sk[r * 32 + lane] = xs[r];
         __syncwarp();
     }

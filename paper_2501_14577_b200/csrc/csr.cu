@@ -14,7 +14,7 @@
 //       a segment depends on scheduling, never a value;
 // and the key side (K9) visits each segment in ascending query position
 // (the records' i are distinct within a segment -- a query selects a key at
-// most once; segments <= 256 are ordered by the key side's register bitonic
+// most once; segments <= KEY_REG_SEG (512) are ordered by the key side's register bitonic
 // sort of (i, position) keys, longer ones by (4) below, a counting sort over a
 // bitmap of query positions into the `order` scratch).  Records are stored as
 // structure-of-arrays, i (4 B) and (A, w) (8 B): the ordering reads only i.  Every f64 sum

@@ -122,11 +122,14 @@ struct CandSet {
         if (c < nruns) {
             const int64_t s0 = causal ? c * M : 0;
             const int64_t len = causal ? min64(M, N - s0) : N;
-            int64_t lo = 0, hi = len;
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (__ldg(scode + s0 + mid) < qc) lo = mid + 1; else hi = mid;
+            // 32-bit ranks (a run is shorter than 2^31) on the run's own base pointer
+            const uint64_t* run = scode + s0;
+            int lo32 = 0, hi32 = (int)len;
+            while (lo32 < hi32) {
+                const int mid = (int)(((unsigned)lo32 + (unsigned)hi32) >> 1);
+                if (__ldg(run + mid) < qc) lo32 = mid + 1; else hi32 = mid;
             }
+            const int64_t lo = lo32;
             const int64_t ww = min64(W, len);
             int64_t st = lo - W / 2;
             st = st < 0 ? 0 : st;
@@ -261,6 +264,10 @@ __device__ __forceinline__ void attend_row(const FwdArgs& a, int64_t bh, int64_t
     const int G = 32 / P;                 // rows per step (1 when nch >= 32)
     const int grp = lane / P, ch_l = lane % P;
     const TV* Vb = static_cast<const TV*>(a.V) + bh * N * (int64_t)a.dv;
+    // d_v/4 a power of two <= 32: one chunk per lane, all lanes active (the unmasked step below also
+    // needs its 4G slots inside one register row: G <= 8)
+    const bool one_pass = P == nch;
+    const TV* Vl = Vb + 4 * ch_l;
     TV* orow = static_cast<TV*>(a.O) + gq * (int64_t)a.dv;
     const float* vbar = a.Vbar + (bh * (a.causal ? N : 1) + mrow) * (int64_t)a.dv;
     const double Amu = Smu * invZ;
@@ -279,6 +286,16 @@ __device__ __forceinline__ void attend_row(const FwdArgs& a, int64_t bh, int64_t
             for (int t0 = 0; t0 < 32 && r * 32 + t0 < nsel; t0 += 4 * G) {
                 float4 v4[4];
                 float A4[4];
+                if (one_pass && G <= 8 && r * 32 + t0 + 4 * G <= nsel) {
+                    // every lane active and every slot of the step selected: lane base + j * d_v
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int src = t0 + u * G + grp;
+                        const int j = __shfl_sync(FULL, jr[r], src);
+                        A4[u] = __shfl_sync(FULL, Ar[r], src);
+                        v4[u] = ld4(Vl + (int64_t)j * a.dv, 0);
+                    }
+                } else {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int src = (t0 + u * G + grp) & 31;
@@ -287,6 +304,7 @@ __device__ __forceinline__ void attend_row(const FwdArgs& a, int64_t bh, int64_t
                     const bool ok = act && t0 + u * G + grp < 32 && r * 32 + t0 + u * G + grp < nsel;
                     v4[u] = ok ? ld4(Vb + (int64_t)j * a.dv, ch) : make_float4(0.f, 0.f, 0.f, 0.f);
                     if (!ok) A4[u] = 0.f;
+                }
                 }
                 acc0 += (double)sum4(A4[0], v4[0].x, A4[1], v4[1].x, A4[2], v4[2].x, A4[3], v4[3].x);
                 acc1 += (double)sum4(A4[0], v4[0].y, A4[1], v4[1].y, A4[2], v4[2].y, A4[3], v4[3].y);

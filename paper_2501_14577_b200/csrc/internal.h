@@ -60,10 +60,14 @@ cudaError_t launch_query_order(const onedf_problem* p, const uint64_t* qcode, in
 
 
 // csr.cu -- A9 key-major CSR of the selected (query, slot) records
-// Segments longer than this are ordered by csr_long_order_kernel (a bitmap over query positions);
-// shorter ones by the key side itself (register bitonic sort of (i << 8 | position) keys).
-constexpr int KEY_REG_SEG = 256;
-constexpr int KEY_POS_BITS = 8;       // the key side's u32 sort key (i << 8 | position) needs N < 2^24
+// Segments longer than this are ordered by csr_long_order_kernel (a bitmap over query positions;
+// none at long64k, where the longest is ~450);
+// shorter ones by the key side itself (register bitonic sort of (i << KEY_POS_BITS | position) keys).
+#ifndef ONEDF_KEY_REG_SEG
+#define ONEDF_KEY_REG_SEG 512
+#endif
+constexpr int KEY_REG_SEG = ONEDF_KEY_REG_SEG;     // 256 or 512 (register rows of the key side's sort)
+constexpr int KEY_POS_BITS = KEY_REG_SEG > 256 ? 9 : 8;   // u32 sort key (i << bits | position): N < 2^(32-bits)
 __host__ __device__ inline bool csr_long_segment(int64_t len, int64_t N) {
     return len > KEY_REG_SEG || N >= (1ll << (32 - KEY_POS_BITS));
 }
