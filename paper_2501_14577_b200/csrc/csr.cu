@@ -58,7 +58,10 @@ __global__ void __launch_bounds__(CSR_THREADS) csr_count_kernel(const int32_t* _
     __shared__ uint32_t tcnt[CSR_TBL];
     const int64_t bh = blockIdx.y;
     const int64_t q0 = (int64_t)blockIdx.x * CSR_QPC;          // schedule slot of the CTA's first query
-    const bool hashed = (int64_t)CSR_QPC * k * 2 <= CSR_TBL;
+#ifndef ONEDF_CSR_HASH
+#define ONEDF_CSR_HASH 1
+#endif
+    const bool hashed = ONEDF_CSR_HASH && (int64_t)CSR_QPC * k * 2 <= CSR_TBL;
     if (hashed) {
         for (int t = threadIdx.x; t < CSR_TBL; t += CSR_THREADS) { tkey[t] = 0u; tcnt[t] = 0u; }
         __syncthreads();

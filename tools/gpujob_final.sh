@@ -17,3 +17,5 @@ python tools/ncu_summary.py /tmp/full_$TAG.ncu-rep --traffic gpurun_out/ncu_traf
   > gpurun_out/ncu_full_${TAG}_summary.txt 2>&1
 if [ "${SWEEP:-1}" = 1 ]; then bash tools/config_sweep.sh > gpurun_out/configs_$TAG.jsonl 2>/dev/null; fi
 echo done
+if [ "${SEQ:-1}" = 1 ]; then timeout 1200 python tools/seqshard_report.py > gpurun_out/seqshard_$TAG.json 2>gpurun_out/seqshard.err; fi
+echo done-all
