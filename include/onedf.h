@@ -215,12 +215,17 @@ onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t*
  *             visited in that order (Morton-adjacent queries share candidate
  *             records and V rows in L1); NULL -> the forward sorts qcode
  *             itself.  Any per-chunk permutation gives bitwise the same outputs.
- *   O, idx, Z outputs (idx/Z are what onedf_topk_attn_bwd consumes). */
+ *   O, idx, Z outputs (idx/Z are what onedf_topk_attn_bwd consumes).
+ *   indeg     nullable output [B,H,N] int32 (caller-owned device memory): the in-degree
+ *             of every key, #{(i, slot): idx[i][slot] == j} over this call's queries
+ *             (A9's counts, exact integers: one atomic add per selected slot in the
+ *             top-k kernel).  Pass it to onedf_topk_attn_bwd with the same idx to skip
+ *             the backward's counting pass over idx. */
 onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K,
                                  const void* V, const float* eps, const uint64_t* qcode,
                                  const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
-                                 void* O, int32_t* idx, float* Z, void* ws, size_t ws_bytes,
-                                 onedf_stream_t stream);
+                                 void* O, int32_t* idx, float* Z, int32_t* indeg, void* ws,
+                                 size_t ws_bytes, onedf_stream_t stream);
 
 /* A8-A12: backward with I held fixed (D16), appendix P:2006-2045 with the
  * dot-product reading D15, the mean-slot chain rule (S:323(a)) and one shared
@@ -240,13 +245,18 @@ onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const f
  *              re-sorting it.  Outputs are bitwise the same.
  *   perm       nullable scheduling hint: onedf_sort's perm.  When given, keys
  *              are visited in sorted-run order; outputs are bitwise the same.
+ *   indeg      nullable: the in-degree counts onedf_topk_attn_fwd wrote for THIS idx
+ *              (same problem, same shard); they size the CSR segments instead of a
+ *              counting pass over idx.  Counts that do not match idx are a caller
+ *              error (records would land in the wrong segments); outputs are bitwise
+ *              the same as with NULL.
  *   dQ, dK     overwritten (f32); dV overwritten (p->vdtype); d_eps device DOUBLE scalar, overwritten with
  *   the sum over all (b,h,i). */
 onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K,
                                  const void* V, const float* eps, const void* O,
                                  const void* dO, const int32_t* idx, const float* Z,
                                  const uint64_t* qcode, const int32_t* qorder, const int32_t* perm,
-                                 float* dQ, float* dK, void* dV, double* d_eps,
+                                 const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps,
                                  void* ws, size_t ws_bytes, onedf_stream_t stream);
 
 /* Instrumented twins of the fwd/bwd calls: identical launches and results,
@@ -261,13 +271,13 @@ onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, 
                                         const void* V, const float* eps, const uint64_t* qcode,
                                         const uint64_t* scode, const int32_t* perm,
                                         const int32_t* qorder, void* O,
-                                        int32_t* idx, float* Z, void* ws, size_t ws_bytes,
+                                        int32_t* idx, float* Z, int32_t* indeg, void* ws, size_t ws_bytes,
                                         void* const* events, int n_events, onedf_stream_t stream);
 onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K,
                                         const void* V, const float* eps, const void* O,
                                         const void* dO, const int32_t* idx, const float* Z,
                                         const uint64_t* qcode, const int32_t* qorder,
-                                        const int32_t* perm,
+                                        const int32_t* perm, const int32_t* indeg,
                                         float* dQ, float* dK, void* dV, double* d_eps,
                                         void* ws, size_t ws_bytes, void* const* events, int n_events,
                                         onedf_stream_t stream);

@@ -62,11 +62,11 @@ def _load():
         "onedf_workspace_size": (sz, [P, i32]),
         "onedf_encode": (i32, [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_sort": (i32, [P, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32, vp]),
-        "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz,
-                                             vp, i32, vp]),
+        "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32, vp]),
+        "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             sz, vp, i32, vp]),
         "onedf_topk_attn_step_host": (i32, [P, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_project_encode": (i32, [P, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz,
                                        vp]),
@@ -151,19 +151,23 @@ def onedf_sort(p, kcode, scode, perm, ws, ws_bytes, stream=None):
            "onedf_sort")
 
 
-def onedf_topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, stream=None):
-    """qorder is a nullable scheduling hint (onedf_sort of the query codes); outputs do not depend on it."""
+def onedf_topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, stream=None,
+                        indeg=None):
+    """qorder is a nullable scheduling hint (onedf_sort of the query codes); outputs do not depend on it.
+    indeg: nullable [B,H,N] int32 output, the keys' in-degree counts for onedf_topk_attn_bwd."""
     _check(_lib.onedf_topk_attn_fwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode), _p(perm),
-                                    _p(qorder), _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, _stream(stream)),
+                                    _p(qorder), _p(O), _p(idx), _p(Z), _p(indeg), _p(ws), ws_bytes,
+                                    _stream(stream)),
            "onedf_topk_attn_fwd")
 
 
 def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws, ws_bytes,
-                        stream=None):
-    """qcode/qorder/perm are nullable scheduling hints (None -> natural order); outputs do not depend on them."""
+                        stream=None, indeg=None):
+    """qcode/qorder/perm are nullable scheduling hints (None -> natural order); outputs do not depend on them.
+    indeg: nullable, the forward's in-degree counts for this idx (skips the counting pass)."""
     _check(_lib.onedf_topk_attn_bwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx), _p(Z),
-                                    _p(qcode), _p(qorder), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps), _p(ws),
-                                    ws_bytes, _stream(stream)),
+                                    _p(qcode), _p(qorder), _p(perm), _p(indeg), _p(dQ), _p(dK), _p(dV), _p(d_eps),
+                                    _p(ws), ws_bytes, _stream(stream)),
            "onedf_topk_attn_bwd")
 
 
@@ -173,19 +177,20 @@ def _events(events):
 
 
 def onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, events,
-                               stream=None):
+                               stream=None, indeg=None):
     arr, n = _events(events)
     _check(_lib.onedf_topk_attn_fwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode),
-                                           _p(perm), _p(qorder), _p(O), _p(idx), _p(Z), _p(ws), ws_bytes, arr, n,
-                                           _stream(stream)), "onedf_topk_attn_fwd_traced")
+                                           _p(perm), _p(qorder), _p(O), _p(idx), _p(Z), _p(indeg), _p(ws), ws_bytes,
+                                           arr, n, _stream(stream)), "onedf_topk_attn_fwd_traced")
 
 
 def onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws,
-                               ws_bytes, events, stream=None):
+                               ws_bytes, events, stream=None, indeg=None):
     arr, n = _events(events)
     _check(_lib.onedf_topk_attn_bwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx),
-                                           _p(Z), _p(qcode), _p(qorder), _p(perm), _p(dQ), _p(dK), _p(dV), _p(d_eps),
-                                           _p(ws), ws_bytes, arr, n, _stream(stream)), "onedf_topk_attn_bwd_traced")
+                                           _p(Z), _p(qcode), _p(qorder), _p(perm), _p(indeg), _p(dQ), _p(dK), _p(dV),
+                                           _p(d_eps), _p(ws), ws_bytes, arr, n, _stream(stream)),
+           "onedf_topk_attn_bwd_traced")
 
 
 def onedf_topk_attn_step_host(p, Q_h, K_h, V_h, eps: float, dO_h, O_h, dQ_h, dK_h, dV_h, d_eps_h, ws, ws_bytes,

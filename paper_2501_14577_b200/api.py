@@ -181,29 +181,34 @@ def query_schedule(p: Problem, qcode, ws: Workspace | None = None):
 
 
 @_on_one_device
-def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | None = None, qorder=None):
+def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | None = None, qorder=None,
+                  indeg=None):
     """A4-A7 -> (O, idx, Z).  V and O are of value_dtype(p); qorder (optional) is the query schedule
-    (query_schedule), which only chooses the visiting order: outputs are bitwise the same without it."""
+    (query_schedule), which only chooses the visiting order: outputs are bitwise the same without it.
+    indeg (optional) is an int32 [B,H,N] tensor the forward fills with the keys' in-degree counts,
+    for topk_attn_bwd(indeg=...)."""
     n = _rows(p)
     Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
     V, eps = _dev(V, value_dtype(p), rows=n, width=p.d_v), _dev(eps, rows=1)
     qorder = None if qorder is None else _dev(qorder, torch.int32, rows=n)
+    indeg = None if indeg is None else _dev(indeg, torch.int32, rows=n)
     O = torch.empty((p.B, p.H, p.N, p.d_v), dtype=value_dtype(p), device=Q.device)
     idx = torch.empty((p.B, p.H, p.N, p.k), dtype=torch.int32, device=Q.device)
     Z = torch.empty((p.B, p.H, p.N), dtype=torch.float32, device=Q.device)
     ptr, nb = _ws(p, abi.OP_FWD, ws)
     abi.onedf_topk_attn_fwd(p, Q, K, V, eps, _dev(qcode, torch.int64, rows=n), _dev(scode, torch.int64, rows=n),
-                            _dev(perm, torch.int32, rows=n), qorder, O, idx, Z, ptr, nb)
+                            _dev(perm, torch.int32, rows=n), qorder, O, idx, Z, ptr, nb, indeg=indeg)
     return O, idx, Z
 
 
 @_on_one_device
 def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None, qcode=None, perm=None,
-                  qorder=None):
+                  qorder=None, indeg=None):
     """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor]); V, O, dO, dV of value_dtype(p).
 
     qcode/qorder/perm (optional) only choose the visiting order (Morton schedule); the
-    outputs are bitwise identical with or without them."""
+    outputs are bitwise identical with or without them.  indeg (optional): the counts
+    topk_attn_fwd(indeg=...) wrote for this idx -- skips the backward's counting pass."""
     n = _rows(p)
     vt = value_dtype(p)
     Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
@@ -218,8 +223,9 @@ def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None 
     qcode = None if qcode is None else _dev(qcode, torch.int64, rows=n)
     qorder = None if qorder is None else _dev(qorder, torch.int32, rows=n)
     perm = None if perm is None else _dev(perm, torch.int32, rows=n)
+    indeg = None if indeg is None else _dev(indeg, torch.int32, rows=n)
     abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32, rows=n, width=p.k), _dev(Z, rows=n), qcode,
-                            qorder, perm, dQ, dK, dV, d_eps, ptr, nb)
+                            qorder, perm, dQ, dK, dV, d_eps, ptr, nb, indeg=indeg)
     return dQ, dK, dV, d_eps
 
 
@@ -287,10 +293,11 @@ class ZetaTopkAttention(torch.autograd.Function):
         qcode, kcode, _ = encode(p, Q, K, ws=ws)
         scode, perm = sort(p, kcode, ws=ws)
         qorder = query_schedule(p, qcode, ws=ws)          # one Morton schedule for both passes
-        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps.reshape(()), qcode, scode, perm, ws=ws, qorder=qorder)
+        indeg = torch.empty((p.B, p.H, p.N), dtype=torch.int32, device=Q.device)   # A9 counts for the backward
+        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps.reshape(()), qcode, scode, perm, ws=ws, qorder=qorder, indeg=indeg)
         if check:
             _raise_on_flags(ws, "ZetaTopkAttention.forward")
-        ctx.save_for_backward(Q, K, V, eps, O, idx, Z, qorder, perm)
+        ctx.save_for_backward(Q, K, V, eps, O, idx, Z, qorder, perm, indeg)
         ctx.p = p
         ctx.check = check
         ctx.mark_non_differentiable(idx)
@@ -298,10 +305,10 @@ class ZetaTopkAttention(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, dO, _didx):
-        Q, K, V, eps, O, idx, Z, qorder, perm = ctx.saved_tensors
+        Q, K, V, eps, O, idx, Z, qorder, perm, indeg = ctx.saved_tensors
         ws = Workspace(Q.device)
         dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps.reshape(()), O, dO.contiguous(), idx, Z, ws=ws,
-                                          qorder=qorder, perm=perm)
+                                          qorder=qorder, perm=perm, indeg=indeg)
         if ctx.check:
             _raise_on_flags(ws, "ZetaTopkAttention.backward")
         return dQ, dK, dV, d_eps.to(eps.dtype).reshape(eps.shape), None, None
@@ -324,8 +331,9 @@ class ZetaProjectedAttention(torch.autograd.Function):
         Q, K, eps, qcode, kcode, _ = project_encode(p, X, Wq, Wk, bq, bk, theta.reshape(()), ws=ws)
         scode, perm = sort(p, kcode, ws=ws)
         qorder = query_schedule(p, qcode, ws=ws)
-        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, ws=ws, qorder=qorder)
-        ctx.save_for_backward(X, Wq, Wk, theta, V, Q, K, eps, O, idx, Z, qorder, perm)
+        indeg = torch.empty((p.B, p.H, p.N), dtype=torch.int32, device=X.device)
+        O, idx, Z = topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, ws=ws, qorder=qorder, indeg=indeg)
+        ctx.save_for_backward(X, Wq, Wk, theta, V, Q, K, eps, O, idx, Z, qorder, perm, indeg)
         ctx.p = p
         ctx.has_bias = (bq is not None, bk is not None)
         ctx.mark_non_differentiable(idx)
@@ -333,10 +341,10 @@ class ZetaProjectedAttention(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, dO, _didx):
-        X, Wq, Wk, theta, V, Q, K, eps, O, idx, Z, qorder, perm = ctx.saved_tensors
+        X, Wq, Wk, theta, V, Q, K, eps, O, idx, Z, qorder, perm, indeg = ctx.saved_tensors
         ws = Workspace(X.device)
         dQ, dK, dV, d_eps = topk_attn_bwd(ctx.p, Q, K, V, eps, O, dO.contiguous(), idx, Z, ws=ws, qorder=qorder,
-                                          perm=perm)
+                                          perm=perm, indeg=indeg)
         dX, dWq, dWk, dbq, dbk, dth = project_bwd(ctx.p, X, Wq, Wk, dQ, dK, theta.reshape(()), d_eps, ws=ws)
         return (dX, dWq, dWk, dbq if ctx.has_bias[0] else None, dbk if ctx.has_bias[1] else None,
                 dth.to(theta.dtype).reshape(theta.shape), dV, None)

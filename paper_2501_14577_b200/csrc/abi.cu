@@ -111,7 +111,7 @@ struct StepLayout {
     char *V, *dO, *O, *dV;          // value rows of the storage type p->vdtype
     double* d_eps;
     uint64_t *qcode, *kcode, *scode;
-    int32_t *perm, *qorder, *idx;
+    int32_t *perm, *qorder, *idx, *indeg;
     size_t sub_off, sub_bytes, bytes;
 };
 static size_t value_bytes(const onedf_problem* p) { return p->vdtype == ONEDF_DTYPE_BF16 ? 2 : 4; }
@@ -130,6 +130,7 @@ static StepLayout step_layout(const onedf_problem* p, void* ws) {
     L.Z = c.take<float>(BH * N); L.eps = c.take<float>(1); L.d_eps = c.take<double>(STEP_GROUPS_MAX + 1);
     L.qcode = c.take<uint64_t>(BH * N); L.kcode = c.take<uint64_t>(BH * N); L.scode = c.take<uint64_t>(BH * N);
     L.perm = c.take<int32_t>(BH * N); L.qorder = c.take<int32_t>(BH * N); L.idx = c.take<int32_t>(BH * N * p->k);
+    L.indeg = c.take<int32_t>(BH * N);
     c.take<char>(0);
     L.sub_off = c.off;
     L.sub_bytes = sub;
@@ -181,27 +182,28 @@ static onedf_status do_sort(const onedf_problem* p, const uint64_t* kcode, uint6
 }
 static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                            const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
-                           void* O, int32_t* idx, float* Z, void* ws, cudaStream_t st, bool zero,
+                           void* O, int32_t* idx, float* Z, int32_t* indeg, void* ws, cudaStream_t st, bool zero,
                            const Trace& tr = Trace()) {
     if (zero && zero_flags(ws, ONEDF_OP_FWD, st) != cudaSuccess) return finish(cudaGetLastError());
     FwdLayout L = fwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
     tr.mark(0, st);
-    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, &L.m, &L.f, ws, st, tr);
+    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, &L.m, &L.f, ws, st, tr);
     return finish(e);
 }
 static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                            const void* dO, const int32_t* idx, const uint64_t* qcode, const int32_t* qorder,
-                           const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, void* ws,
-                           cudaStream_t st, bool zero, const Trace& tr = Trace()) {
+                           const int32_t* perm, const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps,
+                           void* ws, cudaStream_t st, bool zero, const Trace& tr = Trace()) {
     if (zero && zero_flags(ws, ONEDF_OP_BWD, st) != cudaSuccess) return finish(cudaGetLastError());
     BwdLayout L = bwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
     tr.mark(0, st);
     if (e == cudaSuccess)
-        e = launch_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st, tr);
+        e = launch_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, indeg, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st,
+                       tr);
     return finish(e);
 }
 
@@ -255,25 +257,25 @@ static bool rows_misaligned(const onedf_problem* p, const void* a, const void* b
 
 onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                  const float* eps, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,
-                                 const int32_t* qorder, void* O, int32_t* idx, float* Z, void* ws, size_t ws_bytes,
-                                 onedf_stream_t stream) {
-    return onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, nullptr,
-                                      0, stream);
+                                 const int32_t* qorder, void* O, int32_t* idx, float* Z, int32_t* indeg, void* ws,
+                                 size_t ws_bytes, onedf_stream_t stream) {
+    return onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, ws, ws_bytes,
+                                      nullptr, 0, stream);
 }
 
 onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                  const float* eps, const void* O, const void* dO, const int32_t* idx, const float* Z,
-                                 const uint64_t* qcode, const int32_t* qorder, const int32_t* perm, float* dQ,
-                                 float* dK, void* dV, double* d_eps, void* ws, size_t ws_bytes,
-                                 onedf_stream_t stream) {
-    return onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws,
-                                      ws_bytes, nullptr, 0, stream);
+                                 const uint64_t* qcode, const int32_t* qorder, const int32_t* perm,
+                                 const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps, void* ws,
+                                 size_t ws_bytes, onedf_stream_t stream) {
+    return onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, indeg, dQ, dK, dV, d_eps,
+                                      ws, ws_bytes, nullptr, 0, stream);
 }
 
 onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                         const float* eps, const uint64_t* qcode, const uint64_t* scode,
                                         const int32_t* perm, const int32_t* qorder, void* O, int32_t* idx, float* Z,
-                                        void* ws, size_t ws_bytes, void* const* events, int n_events,
+                                        int32_t* indeg, void* ws, size_t ws_bytes, void* const* events, int n_events,
                                         onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_FWD);
     if (s != ONEDF_OK) return s;
@@ -282,14 +284,15 @@ onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, 
     Trace tr;
     tr.ev = events;
     tr.n = n_events;
-    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, (cudaStream_t)stream, true, tr);
+    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, ws, (cudaStream_t)stream, true, tr);
 }
 
 onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                         const float* eps, const void* O, const void* dO, const int32_t* idx,
                                         const float* Z, const uint64_t* qcode, const int32_t* qorder,
-                                        const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, void* ws,
-                                        size_t ws_bytes, void* const* events, int n_events, onedf_stream_t stream) {
+                                        const int32_t* perm, const int32_t* indeg, float* dQ, float* dK, void* dV,
+                                        double* d_eps, void* ws, size_t ws_bytes, void* const* events, int n_events,
+                                        onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_BWD);
     if (s != ONEDF_OK) return s;
     // O and Z are part of the interface but not read (reading R3: recomputed in f64)
@@ -299,8 +302,8 @@ onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, 
     Trace tr;
     tr.ev = events;
     tr.n = n_events;
-    return do_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream, true,
-                  tr);
+    return do_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, indeg, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream,
+                  true, tr);
 }
 
 onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h, const void* V_h,
@@ -362,11 +365,12 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
         // the Morton query schedule, sorted once for both passes
         if ((s = do_sort(&pg, L.qcode + o1, nullptr, L.qorder + o1, sub, st)) != ONEDF_OK) break;
         if ((s = do_fwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.qcode + o1, L.scode + o1, L.perm + o1,
-                        L.qorder + o1, L.O + ov, L.idx + o1 * p->k, L.Z + o1, sub, st, false)) != ONEDF_OK)
+                        L.qorder + o1, L.O + ov, L.idx + o1 * p->k, L.Z + o1, L.indeg + o1, sub, st, false)) !=
+            ONEDF_OK)
             break;
         if ((s = do_bwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.dO + ov, L.idx + o1 * p->k, L.qcode + o1,
-                        L.qorder + o1, L.perm + o1, L.dQ + ok, L.dK + ok, L.dV + ov, L.d_eps + 1 + g, sub, st,
-                        false)) != ONEDF_OK)
+                        L.qorder + o1, L.perm + o1, L.indeg + o1, L.dQ + ok, L.dK + ok, L.dV + ov, L.d_eps + 1 + g,
+                        sub, st, false)) != ONEDF_OK)
             break;
         e = cudaEventRecord(ev_c[g], st);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev_c[g], 0);

@@ -86,8 +86,8 @@ static int lanes_per_row(int dv) {
 
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                        const void* dO, const int32_t* idx, const uint64_t* qcode, const int32_t* qorder,
-                       const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, const MeanBufs* m,
-                       BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr) {
+                       const int32_t* perm, const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps,
+                       const MeanBufs* m, BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
     cudaError_t e = cudaSuccess;
     if (!qorder && qcode) {
@@ -97,7 +97,7 @@ cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, c
         qorder = b->qorder;
     }
     // A9 first: in-degree counts -> CSR offsets + insertion cursors (the query side appends into them)
-    e = launch_csr_count(p, idx, qorder, t, st);
+    e = launch_csr_count(p, idx, qorder, indeg, t, st);
     if (e != cudaSuccess) return e;
     tr.mark(1, st);
     BwdArgs a;

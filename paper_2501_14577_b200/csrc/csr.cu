@@ -317,15 +317,17 @@ cudaError_t launch_csr_long_order(const onedf_problem* p, CsrBufs* t, cudaStream
     return cudaGetLastError();
 }
 
-cudaError_t launch_csr_count(const onedf_problem* p, const int32_t* idx, const int32_t* qorder, CsrBufs* t,
-                             cudaStream_t st) {
+cudaError_t launch_csr_count(const onedf_problem* p, const int32_t* idx, const int32_t* qorder,
+                             const int32_t* indeg, CsrBufs* t, cudaStream_t st) {
     const int64_t BH = p->B * p->H, N = p->N;
-    cudaError_t e = cudaMemsetAsync(t->cursor, 0, (size_t)(BH * N) * sizeof(int32_t), st);
+    cudaError_t e = indeg ? cudaMemcpyAsync(t->cursor, indeg, (size_t)(BH * N) * sizeof(int32_t),
+                                            cudaMemcpyDeviceToDevice, st)
+                          : cudaMemsetAsync(t->cursor, 0, (size_t)(BH * N) * sizeof(int32_t), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(t->nlong, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     const Shard sh = make_shard(p);
     const int64_t nq = sh.slots(N);
-    if (nq > 0) {
+    if (nq > 0 && !indeg) {
         const dim3 grid((unsigned)((nq + CSR_QPC - 1) / CSR_QPC), (unsigned)BH);
         csr_count_kernel<<<grid, CSR_THREADS, 0, st>>>(idx, qorder, N, nq, p->k, sh, t->cursor);
     }

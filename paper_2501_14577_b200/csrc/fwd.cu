@@ -44,6 +44,7 @@ void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f) {
     f->recs = c->take<float>((size_t)(BH * p->N * rec));
     f->qorder = c->take<int32_t>((size_t)(BH * p->N));
     sort_carve(p, c, &f->scr);
+
 }
 
 // ------------------------------------------------------------------ K4
@@ -68,8 +69,8 @@ __global__ void build_records_kernel(const float* __restrict__ K, const int32_t*
 
 cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                        const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
-                       void* O, int32_t* idx, float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st,
-                       const Trace& tr) {
+                       void* O, int32_t* idx, float* Z, int32_t* indeg, const MeanBufs* m, FwdBufs* f, void* ws,
+                       cudaStream_t st, const Trace& tr) {
     const int64_t BH = p->B * p->H, N = p->N, total = BH * N;
     ONEDF_DISPATCH_DK(p->d_k, {
         build_records_kernel<DK><<<(unsigned)((total + 255) / 256), 256, 0, st>>>(K, perm, f->recs, N, total);
@@ -90,6 +91,13 @@ cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, c
     a.N = N; a.M = p->causal ? p->chunk : N; a.total = BH * a.nq;
     a.k = p->k; a.W = effective_window(p); a.dv = p->d_v; a.causal = p->causal; a.mean_slot = p->mean_slot;
     a.score = p->score;
+    a.indeg = indeg;
+    if (indeg) {
+        // A9's in-degree counts, accumulated by the top-k kernel (one integer RED per selected
+        // slot) for the backward to reuse instead of re-reading idx
+        const cudaError_t e = cudaMemsetAsync(indeg, 0, (size_t)(BH * N) * sizeof(int32_t), st);
+        if (e != cudaSuccess) return e;
+    }
     a.ws = ws;
     const int64_t per_cta = (int64_t)FWD_WARPS * FWD_QPW;
     const unsigned grid = (unsigned)((a.total + per_cta - 1) / per_cta);

@@ -99,6 +99,7 @@ struct FwdArgs {
     void* O; int32_t* idx; float* Z;
     int64_t N, M, total, nq;     // nq: schedule slots per (b,h) (N, or the owned chunks when sharded)
     int k, W, dv, causal, mean_slot, score;
+    int32_t* indeg;              // nullable [BH][N]: in-degree counts of the selected keys (A9), += 1 per slot
     Shard sh;
     void* ws;
 };
@@ -537,6 +538,7 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
             const bool valid = e2 < k && top[r] != KEY_MAX;
             jr[r] = valid ? (int)(unsigned)(top[r] & 0xffffffffull) : -1;
             if (e2 < k) idx_row[e2] = jr[r];
+            if (a.indeg && valid) atomicAdd(a.indeg + bh * N + jr[r], 1);
             nsel += __popc(__ballot_sync(FULL, valid));
         }
 
@@ -708,6 +710,7 @@ __global__ void __launch_bounds__(FWD_THREADS) code_select_attn_kernel(const Fwd
         for (int r = 0; r < R; ++r) {
             const int e2 = r * 32 + lane;
             jr[r] = e2 < k ? idx_row[e2] : -1;
+            if (a.indeg && jr[r] >= 0) atomicAdd(a.indeg + bh * N + jr[r], 1);
             nsel += __popc(__ballot_sync(FULL, jr[r] >= 0));
         }
         attend_row<DK, R, TV>(a, bh, i, gq, q, jr, nsel, ed);

@@ -83,9 +83,10 @@ struct CsrBufs {
     int32_t* bsum;      // [BH][N/4096 + 1] block sums of the multi-CTA offset scan
 };
 void csr_carve(const onedf_problem* p, Carver* c, CsrBufs* t);
-// qorder: the query schedule (nullable -> natural order); only its grouping of similar queries matters
-cudaError_t launch_csr_count(const onedf_problem* p, const int32_t* idx, const int32_t* qorder, CsrBufs* t,
-                             cudaStream_t st);
+// qorder: the query schedule (nullable -> natural order); only its grouping of similar queries matters.
+// indeg: nullable, the forward's in-degree counts of this idx (then copied instead of counted)
+cudaError_t launch_csr_count(const onedf_problem* p, const int32_t* idx, const int32_t* qorder,
+                             const int32_t* indeg, CsrBufs* t, cudaStream_t st);
 // after the query side has appended every record: ascending-i order of each long segment
 cudaError_t launch_csr_long_order(const onedf_problem* p, CsrBufs* t, cudaStream_t st);
 
@@ -115,8 +116,8 @@ void fwd_carve(const onedf_problem* p, Carver* c, FwdBufs* f);
 // qorder: the caller's query schedule (nullable -> sorted here from qcode)
 cudaError_t launch_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                        const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
-                       void* O, int32_t* idx, float* Z, const MeanBufs* m, FwdBufs* f, void* ws, cudaStream_t st,
-                       const Trace& tr);
+                       void* O, int32_t* idx, float* Z, int32_t* indeg, const MeanBufs* m, FwdBufs* f, void* ws,
+                       cudaStream_t st, const Trace& tr);
 
 // bwd.cu
 constexpr int EPS_PARTS = 1024;   // fixed first-level split of the d_eps reduction
@@ -131,8 +132,8 @@ struct BwdBufs {
 void bwd_carve(const onedf_problem* p, Carver* c, BwdBufs* b);
 cudaError_t launch_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                        const void* dO, const int32_t* idx, const uint64_t* qcode, const int32_t* qorder,
-                       const int32_t* perm, float* dQ, float* dK, void* dV, double* d_eps, const MeanBufs* m,
-                       BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr);
+                       const int32_t* perm, const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps,
+                       const MeanBufs* m, BwdBufs* b, CsrBufs* t, void* ws, cudaStream_t st, const Trace& tr);
 
 // proj.cu (NEXT-4 projections f_q, f_k and eps = sigma(theta))
 size_t project_ws_bytes(const onedf_problem* p, int d_model, Carver* c);
