@@ -6,7 +6,9 @@
 // queries that selected it, in a FIXED order.  Built in three steps:
 //   (1) in-degree count: cnt[j] += 1 for every valid idx entry (integer
 //       atomics: the counts, and everything derived from them, are exact and
-//       order-free);
+//       order-free) -- done by the forward's top-k kernel (one RED per selected
+//       slot into the caller's indeg, copied here) or, without it, by the
+//       counting pass over idx below;
 //   (2) exclusive scan per (b,h) -> CSR offsets off[j] (and the insertion
 //       cursors, a copy of off), multi-CTA;
 //   (3) the query side (bwd.cu K7) appends each record at
