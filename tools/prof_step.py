@@ -35,13 +35,14 @@ def main():
     dO = torch.randn(*shp, p.d_v, device=dev, generator=g)
     eps = torch.tensor(0.5, device=dev)
     ws = onedf.Workspace(dev)
+    indeg = torch.empty(shp, dtype=torch.int32, device=dev)     # the forward's A9 counts, as in bench.py
     for _ in range(a.steps):            # the launches of bench.py's step
         qc, kc, _ = onedf.encode(p, Q, K, ws=ws)
         sc, pm = onedf.sort(p, kc, ws=ws)
         qo = onedf.query_schedule(p, qc, ws=ws)
-        O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws, qorder=qo)
+        O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws, qorder=qo, indeg=indeg)
         if not a.fwd_only:
-            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qorder=qo, perm=pm)
+            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qorder=qo, perm=pm, indeg=indeg)
     torch.cuda.synchronize()
     print("done", a.config)
 
