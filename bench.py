@@ -370,6 +370,14 @@ def run_gpu(args, cfg, world, rank, local):
     def ptr(tn, g, width=1):
         return tn.data_ptr() + gofs[g] * N * width * tn.element_size()
 
+    # the forward's prefix means for the backward: group g's own region (onedf_means_floats of its problem)
+    mfl = [abi.onedf_means_floats(q) for q in pg]
+    moffs = [sum(mfl[:g]) for g in range(G)]
+    means = torch.empty(max(1, sum(mfl)), device=dev)
+
+    def mptr(g):
+        return means.data_ptr() + moffs[g] * 4 if mfl[g] else None
+
     def step(evg):
         for g in range(G):
             ev, q = evg[g], pg[g]
@@ -383,10 +391,12 @@ def run_gpu(args, cfg, world, rank, local):
             abi.onedf_sort(q, qc, None, qo, ws, need, stream)      # Morton query schedule for fwd and bwd
             ev[2].record(stream)
             abi.onedf_topk_attn_fwd_traced(q, tq, tk, tv, eps, qc, sc, pm, qo, ptr(O, g, cfg.d_v), ptr(idx, g, cfg.k),
-                                           ptr(Z, g), ws, need, ev[3:6], stream, indeg=ptr(indeg, g))
+                                           ptr(Z, g), ws, need, ev[3:6], stream, indeg=ptr(indeg, g),
+                                           means=mptr(g))
             abi.onedf_topk_attn_bwd_traced(q, tq, tk, tv, eps, ptr(O, g, cfg.d_v), tdo, ptr(idx, g, cfg.k), ptr(Z, g),
                                            qc, qo, pm, ptr(dQ, g, cfg.d_k), ptr(dK, g, cfg.d_k), ptr(dV, g, cfg.d_v),
-                                           d_eps.data_ptr() + 8 * g, ws, need, ev[6:12], stream, indeg=ptr(indeg, g))
+                                           d_eps.data_ptr() + 8 * g, ws, need, ev[6:12], stream, indeg=ptr(indeg, g),
+                                           means=mptr(g))
             if world > 1 and G == 1:
                 odist.combine_d_eps(d_eps[0])   # one f64 per rank, rank-ordered sum (D20)
             ev[12].record(stream)
@@ -530,15 +540,15 @@ def count_launches(p) -> int:
     list in profiles/): encode 2 (bounds partials, encode); 2 sorts (key runs, Morton query
     schedule shared by fwd and bwd), each 1 launch for runs <= 8192 keys else the onesweep's
     histogram + bases + one launch per 8-bit digit; fwd: prefix means 6 (mean slot), key records 1,
-    top-k 1 (which also counts the keys' in-degrees); bwd: prefix means 6, CSR offset scan 3 (block
-    sums, their scan, apply; the counts come from the forward), query side 1, long-segment order 1,
-    key side 1, mean-slot scans 6, eps 2."""
+    top-k 1 (which also counts the keys' in-degrees); bwd: CSR offset scan 3 (block sums, their scan,
+    apply; the counts and the prefix means come from the forward), query side 1, long-segment order
+    1, key side 1, mean-slot scans 6, eps 2."""
     means = 6 if p.mean_slot else 0
     run = p.N if not p.causal else min(p.chunk, p.N)
     bits = p.d_k * (p.bits or min(63 // p.d_k, 32))
     sort = 1 if run <= 8192 else 2 + (bits + 7) // 8
     fwd = means + 2
-    bwd = means + 3 + 1 + 1 + 1 + means + 2
+    bwd = 3 + 1 + 1 + 1 + means + 2
     return 2 + 2 * sort + fwd + bwd
 
 

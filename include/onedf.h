@@ -220,12 +220,19 @@ onedf_status onedf_sort(const onedf_problem* p, const uint64_t* kcode, uint64_t*
  *             of every key, #{(i, slot): idx[i][slot] == j} over this call's queries
  *             (A9's counts, exact integers: one atomic add per selected slot in the
  *             top-k kernel).  Pass it to onedf_topk_attn_bwd with the same idx to skip
- *             the backward's counting pass over idx. */
+ *             the backward's counting pass over idx.
+ *   means     nullable output, caller-owned device memory of onedf_means_floats(p) f32:
+ *             the inclusive prefix means of A4 (D8) -- Kbar [B,H,rows,d_k] followed by
+ *             Vbar [B,H,rows,d_v], rows = N (causal) or 1 -- written there instead of the
+ *             workspace.  Pass it to onedf_topk_attn_bwd (same K, V) to skip recomputing
+ *             them.  Ignored when mean_slot == 0. */
 onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K,
                                  const void* V, const float* eps, const uint64_t* qcode,
                                  const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
-                                 void* O, int32_t* idx, float* Z, int32_t* indeg, void* ws,
-                                 size_t ws_bytes, onedf_stream_t stream);
+                                 void* O, int32_t* idx, float* Z, int32_t* indeg, float* means,
+                                 void* ws, size_t ws_bytes, onedf_stream_t stream);
+/* Floats of the `means` buffer: B*H*rows*(d_k + d_v) (0 when mean_slot == 0). */
+int64_t onedf_means_floats(const onedf_problem* p);
 
 /* A8-A12: backward with I held fixed (D16), appendix P:2006-2045 with the
  * dot-product reading D15, the mean-slot chain rule (S:323(a)) and one shared
@@ -250,14 +257,17 @@ onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const f
  *              counting pass over idx.  Counts that do not match idx are a caller
  *              error (records would land in the wrong segments); outputs are bitwise
  *              the same as with NULL.
+ *   means      nullable: the prefix means onedf_topk_attn_fwd wrote for the same K, V
+ *              (read only); NULL recomputes them.  Outputs are bitwise the same.
  *   dQ, dK     overwritten (f32); dV overwritten (p->vdtype); d_eps device DOUBLE scalar, overwritten with
  *   the sum over all (b,h,i). */
 onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K,
                                  const void* V, const float* eps, const void* O,
                                  const void* dO, const int32_t* idx, const float* Z,
                                  const uint64_t* qcode, const int32_t* qorder, const int32_t* perm,
-                                 const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps,
-                                 void* ws, size_t ws_bytes, onedf_stream_t stream);
+                                 const int32_t* indeg, const float* means, float* dQ, float* dK,
+                                 void* dV, double* d_eps, void* ws, size_t ws_bytes,
+                                 onedf_stream_t stream);
 
 /* Instrumented twins of the fwd/bwd calls: identical launches and results,
  * plus cudaEventRecord(events[s], stream) right after internal stage s
@@ -271,13 +281,14 @@ onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, 
                                         const void* V, const float* eps, const uint64_t* qcode,
                                         const uint64_t* scode, const int32_t* perm,
                                         const int32_t* qorder, void* O,
-                                        int32_t* idx, float* Z, int32_t* indeg, void* ws, size_t ws_bytes,
-                                        void* const* events, int n_events, onedf_stream_t stream);
+                                        int32_t* idx, float* Z, int32_t* indeg, float* means, void* ws,
+                                        size_t ws_bytes, void* const* events, int n_events,
+                                        onedf_stream_t stream);
 onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K,
                                         const void* V, const float* eps, const void* O,
                                         const void* dO, const int32_t* idx, const float* Z,
                                         const uint64_t* qcode, const int32_t* qorder,
-                                        const int32_t* perm, const int32_t* indeg,
+                                        const int32_t* perm, const int32_t* indeg, const float* means,
                                         float* dQ, float* dK, void* dV, double* d_eps,
                                         void* ws, size_t ws_bytes, void* const* events, int n_events,
                                         onedf_stream_t stream);

@@ -11,7 +11,8 @@ from .abi import (DTYPE_BF16, DTYPE_F32, OK, OP_BWD, OP_ENCODE, OP_FWD, OP_SORT,
                   onedf_version, onedf_workspace_size, status_string)
 from .api import (HostStep, Workspace, ZetaTopkAttention, bounds_finish, bounds_partial,  # noqa: F401
                   ZetaProjectedAttention, check_device_status, code_knn, default_chunk, encode, make_problem, overlap,
-                  project_bwd, project_encode, query_schedule, rank_sum, sort, topk_attn_bwd, topk_attn_fwd,
+                  means_floats, project_bwd, project_encode, query_schedule, rank_sum, sort, topk_attn_bwd,
+                  topk_attn_fwd,
                   value_dtype, zeta_attention, zeta_projected_attention)
 
 __version__ = "0.1.0"

@@ -62,11 +62,14 @@ def _load():
         "onedf_workspace_size": (sz, [P, i32]),
         "onedf_encode": (i32, [P, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_sort": (i32, [P, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
-        "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32, vp]),
+        "onedf_topk_attn_fwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "onedf_topk_attn_bwd": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz,
+                                      vp]),
+        "onedf_topk_attn_fwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, i32,
+                                             vp]),
         "onedf_topk_attn_bwd_traced": (i32, [P, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                                             sz, vp, i32, vp]),
+                                             vp, sz, vp, i32, vp]),
+        "onedf_means_floats": (ctypes.c_int64, [P]),
         "onedf_topk_attn_step_host": (i32, [P, vp, vp, vp, ctypes.c_float, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "onedf_project_encode": (i32, [P, ctypes.c_int32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz,
                                        vp]),
@@ -90,7 +93,7 @@ def _load():
 
 
 _lib = _load()
-EXPORTS = ("onedf_validate", "onedf_max_run_length", "onedf_workspace_size", "onedf_encode", "onedf_sort",
+EXPORTS = ("onedf_validate", "onedf_max_run_length", "onedf_means_floats", "onedf_workspace_size", "onedf_encode", "onedf_sort",
            "onedf_topk_attn_fwd", "onedf_topk_attn_bwd", "onedf_topk_attn_fwd_traced",
            "onedf_topk_attn_bwd_traced", "onedf_topk_attn_step_host",
            "onedf_project_encode", "onedf_project_workspace_size", "onedf_project_bwd",
@@ -132,6 +135,11 @@ def onedf_validate(p: Problem) -> int:
     return _lib.onedf_validate(ctypes.byref(p))
 
 
+def onedf_means_floats(p) -> int:
+    """Floats of the prefix-means buffer (Kbar then Vbar) that the fwd can hand to the bwd."""
+    return int(_lib.onedf_means_floats(ctypes.byref(p)))
+
+
 def onedf_max_run_length() -> int:
     return _lib.onedf_max_run_length()
 
@@ -152,22 +160,24 @@ def onedf_sort(p, kcode, scode, perm, ws, ws_bytes, stream=None):
 
 
 def onedf_topk_attn_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, stream=None,
-                        indeg=None):
+                        indeg=None, means=None):
     """qorder is a nullable scheduling hint (onedf_sort of the query codes); outputs do not depend on it.
-    indeg: nullable [B,H,N] int32 output, the keys' in-degree counts for onedf_topk_attn_bwd."""
+    indeg: nullable [B,H,N] int32 output, the keys' in-degree counts for onedf_topk_attn_bwd;
+    means: nullable f32 output of onedf_means_floats(p) floats, the prefix means for the backward."""
     _check(_lib.onedf_topk_attn_fwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode), _p(perm),
-                                    _p(qorder), _p(O), _p(idx), _p(Z), _p(indeg), _p(ws), ws_bytes,
+                                    _p(qorder), _p(O), _p(idx), _p(Z), _p(indeg), _p(means), _p(ws), ws_bytes,
                                     _stream(stream)),
            "onedf_topk_attn_fwd")
 
 
 def onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws, ws_bytes,
-                        stream=None, indeg=None):
+                        stream=None, indeg=None, means=None):
     """qcode/qorder/perm are nullable scheduling hints (None -> natural order); outputs do not depend on them.
-    indeg: nullable, the forward's in-degree counts for this idx (skips the counting pass)."""
+    indeg: nullable, the forward's in-degree counts for this idx (skips the counting pass);
+    means: nullable, the forward's prefix means of the same K, V (skips recomputing them)."""
     _check(_lib.onedf_topk_attn_bwd(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx), _p(Z),
-                                    _p(qcode), _p(qorder), _p(perm), _p(indeg), _p(dQ), _p(dK), _p(dV), _p(d_eps),
-                                    _p(ws), ws_bytes, _stream(stream)),
+                                    _p(qcode), _p(qorder), _p(perm), _p(indeg), _p(means), _p(dQ), _p(dK), _p(dV),
+                                    _p(d_eps), _p(ws), ws_bytes, _stream(stream)),
            "onedf_topk_attn_bwd")
 
 
@@ -177,19 +187,19 @@ def _events(events):
 
 
 def onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, ws, ws_bytes, events,
-                               stream=None, indeg=None):
+                               stream=None, indeg=None, means=None):
     arr, n = _events(events)
     _check(_lib.onedf_topk_attn_fwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(qcode), _p(scode),
-                                           _p(perm), _p(qorder), _p(O), _p(idx), _p(Z), _p(indeg), _p(ws), ws_bytes,
-                                           arr, n, _stream(stream)), "onedf_topk_attn_fwd_traced")
+                                           _p(perm), _p(qorder), _p(O), _p(idx), _p(Z), _p(indeg), _p(means), _p(ws),
+                                           ws_bytes, arr, n, _stream(stream)), "onedf_topk_attn_fwd_traced")
 
 
 def onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, dQ, dK, dV, d_eps, ws,
-                               ws_bytes, events, stream=None, indeg=None):
+                               ws_bytes, events, stream=None, indeg=None, means=None):
     arr, n = _events(events)
     _check(_lib.onedf_topk_attn_bwd_traced(ctypes.byref(p), _p(Q), _p(K), _p(V), _p(eps), _p(O), _p(dO), _p(idx),
-                                           _p(Z), _p(qcode), _p(qorder), _p(perm), _p(indeg), _p(dQ), _p(dK), _p(dV),
-                                           _p(d_eps), _p(ws), ws_bytes, arr, n, _stream(stream)),
+                                           _p(Z), _p(qcode), _p(qorder), _p(perm), _p(indeg), _p(means), _p(dQ),
+                                           _p(dK), _p(dV), _p(d_eps), _p(ws), ws_bytes, arr, n, _stream(stream)),
            "onedf_topk_attn_bwd_traced")
 
 

@@ -71,6 +71,11 @@ def _dev(t: torch.Tensor, dtype=torch.float32, rows: int | None = None, width: i
     return t
 
 
+def means_floats(p: Problem) -> int:
+    """Elements of the f32 prefix-means tensor topk_attn_fwd(means=...) fills (0 without the mean slot)."""
+    return abi.onedf_means_floats(p)
+
+
 def _rows(p: Problem) -> int:
     return p.B * p.H * p.N
 
@@ -182,33 +187,37 @@ def query_schedule(p: Problem, qcode, ws: Workspace | None = None):
 
 @_on_one_device
 def topk_attn_fwd(p: Problem, Q, K, V, eps, qcode, scode, perm, ws: Workspace | None = None, qorder=None,
-                  indeg=None):
+                  indeg=None, means=None):
     """A4-A7 -> (O, idx, Z).  V and O are of value_dtype(p); qorder (optional) is the query schedule
     (query_schedule), which only chooses the visiting order: outputs are bitwise the same without it.
     indeg (optional) is an int32 [B,H,N] tensor the forward fills with the keys' in-degree counts,
-    for topk_attn_bwd(indeg=...)."""
+    for topk_attn_bwd(indeg=...); means (optional) an f32 tensor of means_floats(p) elements that receives
+    the prefix means, for topk_attn_bwd(means=...)."""
     n = _rows(p)
     Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
     V, eps = _dev(V, value_dtype(p), rows=n, width=p.d_v), _dev(eps, rows=1)
     qorder = None if qorder is None else _dev(qorder, torch.int32, rows=n)
     indeg = None if indeg is None else _dev(indeg, torch.int32, rows=n)
+    means = None if means is None else _dev(means, rows=abi.onedf_means_floats(p))
     O = torch.empty((p.B, p.H, p.N, p.d_v), dtype=value_dtype(p), device=Q.device)
     idx = torch.empty((p.B, p.H, p.N, p.k), dtype=torch.int32, device=Q.device)
     Z = torch.empty((p.B, p.H, p.N), dtype=torch.float32, device=Q.device)
     ptr, nb = _ws(p, abi.OP_FWD, ws)
     abi.onedf_topk_attn_fwd(p, Q, K, V, eps, _dev(qcode, torch.int64, rows=n), _dev(scode, torch.int64, rows=n),
-                            _dev(perm, torch.int32, rows=n), qorder, O, idx, Z, ptr, nb, indeg=indeg)
+                            _dev(perm, torch.int32, rows=n), qorder, O, idx, Z, ptr, nb, indeg=indeg,
+                            means=means)
     return O, idx, Z
 
 
 @_on_one_device
 def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None = None, qcode=None, perm=None,
-                  qorder=None, indeg=None):
+                  qorder=None, indeg=None, means=None):
     """A8-A12 -> (dQ, dK, dV, d_eps[float64 scalar tensor]); V, O, dO, dV of value_dtype(p).
 
     qcode/qorder/perm (optional) only choose the visiting order (Morton schedule); the
     outputs are bitwise identical with or without them.  indeg (optional): the counts
-    topk_attn_fwd(indeg=...) wrote for this idx -- skips the backward's counting pass."""
+    topk_attn_fwd(indeg=...) wrote for this idx -- skips the backward's counting pass; means (optional):
+    the prefix means topk_attn_fwd(means=...) wrote for the same K, V -- skips recomputing them."""
     n = _rows(p)
     vt = value_dtype(p)
     Q, K = _dev(Q, rows=n, width=p.d_k), _dev(K, rows=n, width=p.d_k)
@@ -224,8 +233,10 @@ def topk_attn_bwd(p: Problem, Q, K, V, eps, O, dO, idx, Z, ws: Workspace | None 
     qorder = None if qorder is None else _dev(qorder, torch.int32, rows=n)
     perm = None if perm is None else _dev(perm, torch.int32, rows=n)
     indeg = None if indeg is None else _dev(indeg, torch.int32, rows=n)
+    means = None if means is None else _dev(means, rows=abi.onedf_means_floats(p))
     abi.onedf_topk_attn_bwd(p, Q, K, V, eps, O, dO, _dev(idx, torch.int32, rows=n, width=p.k), _dev(Z, rows=n), qcode,
-                            qorder, perm, dQ, dK, dV, d_eps, ptr, nb, indeg=indeg)
+                            qorder, perm, dQ, dK, dV, d_eps, ptr, nb, indeg=indeg,
+                            means=means)
     return dQ, dK, dV, d_eps
 
 

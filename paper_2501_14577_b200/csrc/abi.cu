@@ -112,6 +112,7 @@ struct StepLayout {
     double* d_eps;
     uint64_t *qcode, *kcode, *scode;
     int32_t *perm, *qorder, *idx, *indeg;
+    float* means;                   // the forward's prefix means, read by the backward
     size_t sub_off, sub_bytes, bytes;
 };
 static size_t value_bytes(const onedf_problem* p) { return p->vdtype == ONEDF_DTYPE_BF16 ? 2 : 4; }
@@ -131,6 +132,8 @@ static StepLayout step_layout(const onedf_problem* p, void* ws) {
     L.qcode = c.take<uint64_t>(BH * N); L.kcode = c.take<uint64_t>(BH * N); L.scode = c.take<uint64_t>(BH * N);
     L.perm = c.take<int32_t>(BH * N); L.qorder = c.take<int32_t>(BH * N); L.idx = c.take<int32_t>(BH * N * p->k);
     L.indeg = c.take<int32_t>(BH * N);
+    // room for every group's means region (each 256-B aligned; groups of fewer slices need no more)
+    L.means = p->mean_slot ? c.take<float>((size_t)(onedf_means_floats(p) + 2 * 64 * STEP_GROUPS_MAX)) : nullptr;
     c.take<char>(0);
     L.sub_off = c.off;
     L.sub_bytes = sub;
@@ -180,26 +183,38 @@ static onedf_status do_sort(const onedf_problem* p, const uint64_t* kcode, uint6
     sort_carve(p, &c, &scr);
     return finish(launch_seg_sort(p, kcode, scode, perm, scr, st));
 }
+// A caller-owned prefix-means buffer (onedf.h: Kbar [B,H,rows,d_k] then Vbar [B,H,rows,d_v], f32).
+// Both blocks start 256-B aligned (the kernels read the rows as float4).
+static int64_t align64(int64_t x) { return (x + 63) / 64 * 64; }
+static void means_view(const onedf_problem* p, float* means, MeanBufs* m) {
+    const int64_t rows = p->causal ? p->N : 1;
+    m->Kbar = means;
+    m->Vbar = means + align64(p->B * p->H * rows * p->d_k);
+}
 static onedf_status do_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                            const uint64_t* qcode, const uint64_t* scode, const int32_t* perm, const int32_t* qorder,
-                           void* O, int32_t* idx, float* Z, int32_t* indeg, void* ws, cudaStream_t st, bool zero,
-                           const Trace& tr = Trace()) {
+                           void* O, int32_t* idx, float* Z, int32_t* indeg, float* means, void* ws, cudaStream_t st,
+                           bool zero, const Trace& tr = Trace()) {
     if (zero && zero_flags(ws, ONEDF_OP_FWD, st) != cudaSuccess) return finish(cudaGetLastError());
     FwdLayout L = fwd_layout(p, ws);
+    if (means) means_view(p, means, &L.m);          // the prefix means land in the caller's buffer
     cudaError_t e = cudaSuccess;
     if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
     tr.mark(0, st);
-    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, &L.m, &L.f, ws, st, tr);
+    if (e == cudaSuccess) e = launch_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, &L.m, &L.f, ws, st,
+                                              tr);
     return finish(e);
 }
 static onedf_status do_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V, const float* eps,
                            const void* dO, const int32_t* idx, const uint64_t* qcode, const int32_t* qorder,
-                           const int32_t* perm, const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps,
-                           void* ws, cudaStream_t st, bool zero, const Trace& tr = Trace()) {
+                           const int32_t* perm, const int32_t* indeg, const float* means, float* dQ, float* dK,
+                           void* dV, double* d_eps, void* ws, cudaStream_t st, bool zero,
+                           const Trace& tr = Trace()) {
     if (zero && zero_flags(ws, ONEDF_OP_BWD, st) != cudaSuccess) return finish(cudaGetLastError());
     BwdLayout L = bwd_layout(p, ws);
     cudaError_t e = cudaSuccess;
-    if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
+    if (means) means_view(p, const_cast<float*>(means), &L.m);   // the forward's prefix means: read only
+    else if (p->mean_slot) e = launch_prefix_means(p, K, V, &L.m, st);
     tr.mark(0, st);
     if (e == cudaSuccess)
         e = launch_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, indeg, dQ, dK, dV, d_eps, &L.m, &L.b, &L.t, ws, st,
@@ -255,28 +270,34 @@ static bool rows_misaligned(const onedf_problem* p, const void* a, const void* b
     return ((((uintptr_t)a) | ((uintptr_t)b) | ((uintptr_t)c)) & m) != 0;
 }
 
+int64_t onedf_means_floats(const onedf_problem* p) {
+    if (!p || !p->mean_slot) return 0;
+    const int64_t rows = p->B * p->H * (p->causal ? p->N : 1);
+    return align64(rows * p->d_k) + align64(rows * p->d_v);
+}
+
 onedf_status onedf_topk_attn_fwd(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                  const float* eps, const uint64_t* qcode, const uint64_t* scode, const int32_t* perm,
-                                 const int32_t* qorder, void* O, int32_t* idx, float* Z, int32_t* indeg, void* ws,
-                                 size_t ws_bytes, onedf_stream_t stream) {
-    return onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, ws, ws_bytes,
-                                      nullptr, 0, stream);
+                                 const int32_t* qorder, void* O, int32_t* idx, float* Z, int32_t* indeg, float* means,
+                                 void* ws, size_t ws_bytes, onedf_stream_t stream) {
+    return onedf_topk_attn_fwd_traced(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, means, ws,
+                                      ws_bytes, nullptr, 0, stream);
 }
 
 onedf_status onedf_topk_attn_bwd(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                  const float* eps, const void* O, const void* dO, const int32_t* idx, const float* Z,
                                  const uint64_t* qcode, const int32_t* qorder, const int32_t* perm,
-                                 const int32_t* indeg, float* dQ, float* dK, void* dV, double* d_eps, void* ws,
-                                 size_t ws_bytes, onedf_stream_t stream) {
-    return onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, indeg, dQ, dK, dV, d_eps,
-                                      ws, ws_bytes, nullptr, 0, stream);
+                                 const int32_t* indeg, const float* means, float* dQ, float* dK, void* dV,
+                                 double* d_eps, void* ws, size_t ws_bytes, onedf_stream_t stream) {
+    return onedf_topk_attn_bwd_traced(p, Q, K, V, eps, O, dO, idx, Z, qcode, qorder, perm, indeg, means, dQ, dK, dV,
+                                      d_eps, ws, ws_bytes, nullptr, 0, stream);
 }
 
 onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                         const float* eps, const uint64_t* qcode, const uint64_t* scode,
                                         const int32_t* perm, const int32_t* qorder, void* O, int32_t* idx, float* Z,
-                                        int32_t* indeg, void* ws, size_t ws_bytes, void* const* events, int n_events,
-                                        onedf_stream_t stream) {
+                                        int32_t* indeg, float* means, void* ws, size_t ws_bytes, void* const* events,
+                                        int n_events, onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_FWD);
     if (s != ONEDF_OK) return s;
     if (!Q || !K || !V || !eps || !qcode || !scode || !perm || !O || !idx || !Z) return ONEDF_ERR_INVALID_ARG;
@@ -284,15 +305,16 @@ onedf_status onedf_topk_attn_fwd_traced(const onedf_problem* p, const float* Q, 
     Trace tr;
     tr.ev = events;
     tr.n = n_events;
-    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, ws, (cudaStream_t)stream, true, tr);
+    return do_fwd(p, Q, K, V, eps, qcode, scode, perm, qorder, O, idx, Z, indeg, means, ws, (cudaStream_t)stream, true,
+                  tr);
 }
 
 onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, const float* K, const void* V,
                                         const float* eps, const void* O, const void* dO, const int32_t* idx,
                                         const float* Z, const uint64_t* qcode, const int32_t* qorder,
-                                        const int32_t* perm, const int32_t* indeg, float* dQ, float* dK, void* dV,
-                                        double* d_eps, void* ws, size_t ws_bytes, void* const* events, int n_events,
-                                        onedf_stream_t stream) {
+                                        const int32_t* perm, const int32_t* indeg, const float* means, float* dQ,
+                                        float* dK, void* dV, double* d_eps, void* ws, size_t ws_bytes,
+                                        void* const* events, int n_events, onedf_stream_t stream) {
     onedf_status s = pre(p, ws, ws_bytes, ONEDF_OP_BWD);
     if (s != ONEDF_OK) return s;
     // O and Z are part of the interface but not read (reading R3: recomputed in f64)
@@ -302,8 +324,8 @@ onedf_status onedf_topk_attn_bwd_traced(const onedf_problem* p, const float* Q, 
     Trace tr;
     tr.ev = events;
     tr.n = n_events;
-    return do_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, indeg, dQ, dK, dV, d_eps, ws, (cudaStream_t)stream,
-                  true, tr);
+    return do_bwd(p, Q, K, V, eps, dO, idx, qcode, qorder, perm, indeg, means, dQ, dK, dV, d_eps, ws,
+                  (cudaStream_t)stream, true, tr);
 }
 
 onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h, const float* K_h, const void* V_h,
@@ -340,7 +362,7 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
     if (e == cudaSuccess) e = cudaEventRecord(ev_start, st);       // prior work on `st` precedes the copies
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sin, ev_start, 0);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, ev_start, 0);
-    int64_t h0 = 0;
+    int64_t h0 = 0, moff = 0;
     for (int g = 0; g < G && e == cudaSuccess; ++g) {
         const int64_t nh = BH / G + (g < BH % G ? 1 : 0);           // slices of group g: [h0, h0 + nh)
         onedf_problem pg = *p;
@@ -349,6 +371,8 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
         const size_t es = value_bytes(p);
         const size_t ok = (size_t)(h0 * N * p->d_k), ov = (size_t)(h0 * N * p->d_v) * es, o1 = (size_t)(h0 * N);
         const size_t bk = (size_t)(nh * N * p->d_k) * 4, bv = (size_t)(nh * N * p->d_v) * es;
+        // group g's prefix means: its own region (onedf_means_floats of the group's problem)
+        float* gmeans = L.means ? L.means + moff : nullptr;
         const char* Vh = static_cast<const char*>(V_h);
         const char* dOh = static_cast<const char*>(dO_h);
         e = cudaMemcpyAsync(L.Q + ok, Q_h + ok, bk, cudaMemcpyHostToDevice, sin);
@@ -365,11 +389,12 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
         // the Morton query schedule, sorted once for both passes
         if ((s = do_sort(&pg, L.qcode + o1, nullptr, L.qorder + o1, sub, st)) != ONEDF_OK) break;
         if ((s = do_fwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.qcode + o1, L.scode + o1, L.perm + o1,
-                        L.qorder + o1, L.O + ov, L.idx + o1 * p->k, L.Z + o1, L.indeg + o1, sub, st, false)) !=
-            ONEDF_OK)
+                        L.qorder + o1, L.O + ov, L.idx + o1 * p->k, L.Z + o1, L.indeg + o1, gmeans, sub, st,
+                        false)) != ONEDF_OK)
             break;
         if ((s = do_bwd(&pg, L.Q + ok, L.K + ok, L.V + ov, L.eps, L.dO + ov, L.idx + o1 * p->k, L.qcode + o1,
-                        L.qorder + o1, L.perm + o1, L.indeg + o1, L.dQ + ok, L.dK + ok, L.dV + ov, L.d_eps + 1 + g,
+                        L.qorder + o1, L.perm + o1, L.indeg + o1, gmeans, L.dQ + ok, L.dK + ok, L.dV + ov,
+                        L.d_eps + 1 + g,
                         sub, st, false)) != ONEDF_OK)
             break;
         e = cudaEventRecord(ev_c[g], st);
@@ -379,6 +404,7 @@ onedf_status onedf_topk_attn_step_host(const onedf_problem* p, const float* Q_h,
         if (e == cudaSuccess) e = cudaMemcpyAsync(dK_h + ok, L.dK + ok, bk, cudaMemcpyDeviceToHost, sout);
         if (e == cudaSuccess) e = cudaMemcpyAsync(static_cast<char*>(dV_h) + ov, L.dV + ov, bv, cudaMemcpyDeviceToHost, sout);
         h0 += nh;
+        moff += onedf_means_floats(&pg);
     }
     if (s == ONEDF_OK && e == cudaSuccess) {
         sum_groups_kernel<<<1, 1, 0, st>>>(L.d_eps, G);

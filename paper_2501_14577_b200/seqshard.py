@@ -108,11 +108,13 @@ def step(p: abi.Problem, Q, K, V, eps, dO=None, ws=None):
     qo = api.query_schedule(p, qc, ws=ws)          # the owned chunks' Morton schedule, for both passes
     yield ("gather_rows", [sc, pm, K, V])          # in place: complete runs and rows on every rank
     indeg = torch.empty((p.B, p.H, p.N), dtype=torch.int32, device=Q.device)   # this rank's queries' A9 counts
-    O, idx, Z = api.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws, qorder=qo, indeg=indeg)
+    means = torch.empty(api.means_floats(p), device=Q.device)                   # and prefix means, for the bwd
+    O, idx, Z = api.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws, qorder=qo, indeg=indeg, means=means)
     out = {"O": O, "idx": idx, "Z": Z, "qcode": qc, "scode": sc, "perm": pm, "lohi": lohi}
     if dO is None:
         return out
-    dQ, dK, dV, d_eps = api.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qorder=qo, perm=pm, indeg=indeg)
+    dQ, dK, dV, d_eps = api.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qorder=qo, perm=pm, indeg=indeg,
+                                          means=means)
     yield ("reduce_rows", [dK, dV])                # in place: owners' rows become the rank-ordered sums
     d_eps = yield ("sum_scalar", d_eps)
     out.update(dQ=dQ, dK=dK, dV=dV, d_eps=d_eps)

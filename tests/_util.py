@@ -30,11 +30,13 @@ def gpu_run(kw: dict, x: dict, eps: float = synth.EPS, bwd: bool = True, lohi=No
     # the forward's in-degree counts feed the backward's CSR (the bench's path; the schedule-hint test
     # checks that the counting backward gives the same bits)
     indeg = torch.empty((p.B, p.H, p.N), dtype=torch.int32, device=dev)
-    O, idx, Z = onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws, qorder=qo, indeg=indeg)
+    means = torch.empty(onedf.means_floats(p), device=dev)       # the forward's prefix means, likewise
+    O, idx, Z = onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws, qorder=qo, indeg=indeg,
+                                    means=means)
     out = dict(qcode=qc, kcode=kc, lohi=lohi_out, scode=sc, perm=pm, O=O, idx=idx, Z=Z)
     if bwd:
         dQ, dK, dV, d_eps = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws,
-                                                qorder=qo, perm=pm, indeg=indeg)
+                                                qorder=qo, perm=pm, indeg=indeg, means=means)
         out.update(dQ=dQ, dK=dK, dV=dV, d_eps=d_eps)
     torch.cuda.synchronize()
     res = {}

@@ -146,10 +146,11 @@ def test_calls_check_arguments_before_any_launch(onedf):
     good = onedf.Problem(*GOOD.values())
     assert lib.onedf_encode(ctypes.byref(bad), 1, 1, None, 1, 1, None, 256, 1 << 30, None) == onedf.abi.ERR_INVALID_ARG
     # workspace too small / misaligned / NULL -> ERR_WORKSPACE (checked before the device)
-    # (fwd: Q..Z, then the nullable indeg; bwd: Q..perm, nullable indeg, dQ..d_eps)
-    assert lib.onedf_topk_attn_fwd(ctypes.byref(good), *([256] * 11), None, 256, 16, None) == onedf.abi.ERR_WORKSPACE
+    # (fwd: Q..Z, then the nullable indeg and means; bwd: Q..perm, nullable indeg and means, dQ..d_eps)
+    assert lib.onedf_topk_attn_fwd(ctypes.byref(good), *([256] * 11), None, None, 256, 16,
+                                   None) == onedf.abi.ERR_WORKSPACE
     assert lib.onedf_sort(ctypes.byref(good), 256, 256, 256, 257, 1 << 20, None) == onedf.abi.ERR_WORKSPACE
-    assert lib.onedf_topk_attn_bwd(ctypes.byref(good), *([256] * 11), None, *([256] * 4), None, 1 << 40,
+    assert lib.onedf_topk_attn_bwd(ctypes.byref(good), *([256] * 11), None, None, *([256] * 4), None, 1 << 40,
                                    None) == onedf.abi.ERR_WORKSPACE
     assert onedf.status_string(onedf.abi.ERR_WORKSPACE).startswith("workspace")
 

@@ -390,14 +390,16 @@ def test_schedule_hints_do_not_change_results(name):
     # the forward's in-degree counts (A9): the exact per-key count of idx entries, and a backward
     # that takes them instead of counting gives the same bits
     indeg = torch.full((p.B, p.H, p.N), -7, dtype=torch.int32, device=dev)
+    means = torch.full((onedf.means_floats(p),), float("nan"), device=dev)
     fwd_c = [v.cpu().numpy() for v in onedf.topk_attn_fwd(p, t["Q"], t["K"], t["V"], e, qc, sc, pm, ws=ws,
-                                                          qorder=qo, indeg=indeg)]
+                                                          qorder=qo, indeg=indeg, means=means)]
     for u, v, n in zip(fwd_a, fwd_c, ("O", "idx", "Z")):
         assert np.array_equal(u.view(np.uint8), v.view(np.uint8)), n
     ix = fwd_a[1].reshape(p.B * p.H, p.N, p.k)
     want = np.stack([np.bincount(r[r >= 0].ravel(), minlength=p.N) for r in ix]).reshape(p.B, p.H, p.N)
     assert_same(indeg.cpu().numpy(), want.astype(np.int32), "indeg")
-    for hints in ({}, {"qorder": qo, "perm": pm}, {"qorder": nat}, {"qorder": qo, "perm": pm, "indeg": indeg}):
+    for hints in ({}, {"qorder": qo, "perm": pm}, {"qorder": nat}, {"qorder": qo, "perm": pm, "indeg": indeg},
+                  {"qorder": qo, "perm": pm, "indeg": indeg, "means": means}, {"means": means}):
         b = onedf.topk_attn_bwd(p, t["Q"], t["K"], t["V"], e, O, t["dO"], idx, Z, ws=ws, **hints)
         b = [v.cpu().numpy() for v in b]
         for u, v, n in zip(a, b, ("dQ", "dK", "dV", "d_eps")):

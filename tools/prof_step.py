@@ -36,13 +36,14 @@ def main():
     eps = torch.tensor(0.5, device=dev)
     ws = onedf.Workspace(dev)
     indeg = torch.empty(shp, dtype=torch.int32, device=dev)     # the forward's A9 counts, as in bench.py
+    means = torch.empty(onedf.means_floats(p), device=dev)      # and its prefix means
     for _ in range(a.steps):            # the launches of bench.py's step
         qc, kc, _ = onedf.encode(p, Q, K, ws=ws)
         sc, pm = onedf.sort(p, kc, ws=ws)
         qo = onedf.query_schedule(p, qc, ws=ws)
-        O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws, qorder=qo, indeg=indeg)
+        O, idx, Z = onedf.topk_attn_fwd(p, Q, K, V, eps, qc, sc, pm, ws=ws, qorder=qo, indeg=indeg, means=means)
         if not a.fwd_only:
-            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qorder=qo, perm=pm, indeg=indeg)
+            onedf.topk_attn_bwd(p, Q, K, V, eps, O, dO, idx, Z, ws=ws, qorder=qo, perm=pm, indeg=indeg, means=means)
     torch.cuda.synchronize()
     print("done", a.config)
 
