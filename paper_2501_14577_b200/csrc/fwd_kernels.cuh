@@ -27,6 +27,10 @@ constexpr int FWD_UB = ONEDF_FWD_UB;                // candidate batches of 32 l
 #define ONEDF_FWD_TBITS 18                          // bisection of T stops at 2^(TBITS-23) relative width
 #endif
 constexpr int FWD_CAP = 256;                        // pass-2 collection capacity per warp
+#ifndef ONEDF_FWD_MULT_NUM
+#define ONEDF_FWD_MULT_NUM 3                        // pass 1 aims at (NUM/DEN) k keys (the sampled bound's margin)
+#define ONEDF_FWD_MULT_DEN 2
+#endif
 #ifndef ONEDF_FWD_SUB
 #define ONEDF_FWD_SUB 4
 #endif
@@ -434,7 +438,8 @@ __global__ void __launch_bounds__(FWD_THREADS, ONEDF_FWD_MINB) topk_attn_fwd_ker
         unsigned tb;
         if (sampled) {
             const int nsub = (int)((cs.nruns + FWD_SUB - 1) / FWD_SUB);
-            const int target = (int)((3 * (int64_t)k * nsub + 2 * cs.nruns - 1) / (2 * cs.nruns));
+            const int target = (int)((ONEDF_FWD_MULT_NUM * (int64_t)k * nsub + ONEDF_FWD_MULT_DEN * cs.nruns - 1) /
+                                     (ONEDF_FWD_MULT_DEN * cs.nruns));
             tb = pass_one(FWD_SUB, target < 1 ? 1 : target);
         } else {
             tb = pass_one(1, k);
